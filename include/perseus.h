@@ -1,0 +1,217 @@
+/*
+ * include/perseus.h — the C-ABI boundary of the B200-native Perseus MoE
+ * expert-parallel layer (libperseus.so).
+ *
+ * The reference (`sigsim`, /root/reference/proj) is a C++20 static library
+ * with no C ABI and no FFI.  Its hot-path operator API lives in
+ * proj/include/sigsim/{workload,protocols,metrics,trace}.hpp.  This header is
+ * the thin, plain-pointer ABI under our C++ drop-in (include/sigsim/ headers) and
+ * under the Python mirror (paper_2605_00686_b200/): every entry point names the
+ * reference interface it replaces.  No torch types, no C++ types cross it.
+ *
+ * Status codes mirror the reference's error taxonomy (sim.hpp:17-28) and its
+ * CLI exit-code contract (tools/main.cpp:6,130-136):
+ *   0 ok | 1 ConfigError | 2 verification/ordering failure | 3 runtime error
+ *   (ModelError, CUDA error, signal-wait timeout).
+ * perseus_last_error() returns the thread-local message of the last failure.
+ */
+#ifndef PERSEUS_H_
+#define PERSEUS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PERSEUS_OK 0
+#define PERSEUS_ERR_CONFIG 1
+#define PERSEUS_ERR_VERIFY 2
+#define PERSEUS_ERR_RUNTIME 3
+
+#define PERSEUS_ABI_VERSION 1
+
+const char* perseus_last_error(void);
+int perseus_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Planner (host).  Same semantics as the reference free functions.
+ * ------------------------------------------------------------------------- */
+
+/* TransferSpec (workload.hpp:42-49), flattened. */
+typedef struct perseus_transfer {
+    uint32_t src_pe;
+    uint32_t dst_pe;
+    int64_t expert;
+    uint64_t bytes;
+    int64_t tile_id; /* globally unique; doubles as the flag-word id */
+    uint64_t heap_offset;
+} perseus_transfer;
+
+/* replaces sigsim::remote_transfer_count (workload.hpp:72, workload.cpp:39-47) */
+int perseus_remote_transfer_count(int64_t experts, int64_t pes, int64_t pes_per_node,
+                                  int64_t* out);
+
+/* replaces sigsim::message_size (workload.hpp:75-76, workload.cpp:49-55) */
+uint64_t perseus_message_size(uint64_t tokens, int64_t top_k, int64_t experts,
+                              int64_t hidden_dim);
+
+/* replaces sigsim::zipf_route (workload.hpp:79-80, workload.cpp:57-97).
+ * counts[E]; ids[S*k] (nullable) receives the per-token draws in draw order. */
+int perseus_zipf_route(uint64_t tokens, int64_t experts, double exponent, int64_t top_k,
+                       uint64_t seed, uint64_t* counts, int32_t* ids);
+
+/* replaces sigsim::build_dispatch (workload.hpp:82-84, workload.cpp:155-213)
+ * and DispatchWorkload::digest (workload.cpp:105-126).  Call with NULL arrays
+ * to size them. */
+int perseus_build_dispatch(int64_t hidden_dim, int64_t intermediate_dim, int64_t experts,
+                           int64_t top_k, int nodes, int gpus_per_node, int num_qps,
+                           uint64_t tokens, double skew, uint64_t tile_bytes, uint64_t seed,
+                           perseus_transfer* remote, size_t remote_cap, size_t* n_remote,
+                           perseus_transfer* local, size_t local_cap, size_t* n_local,
+                           uint64_t* workload_digest);
+
+/* replaces sigsim::assign_groups (protocols.hpp:58-59, protocols.cpp:52-94).
+ * group_of[n]; leaders[n_groups] (nullable). */
+int perseus_assign_groups(const perseus_transfer* transfers, size_t n, int64_t group_size,
+                          int64_t* group_of, int64_t* leaders, size_t* n_groups);
+
+/* replaces SymmetricHeap::digest (transport.hpp:130-156, transport.cpp:26-43):
+ * extents[n_ext*3] = (pe, offset, length); flags[n_flags]. */
+uint64_t perseus_heap_digest(const uint64_t* extents, size_t n_ext, const uint64_t* flags,
+                             size_t n_flags);
+
+/* replaces sigsim::fnv1a64 (trace.hpp:67, trace.cpp:53-62) */
+uint64_t perseus_fnv1a64(const void* data, size_t len, uint64_t h);
+
+/* ---------------------------------------------------------------------------
+ * Layer (device).  One handle per (process, GPU, EP rank).
+ *
+ * replaces the reference's hot path run_dispatch (protocols.hpp:62-64,
+ * protocols.cpp:346-362) — which only simulates the dispatch puts/signals and
+ * stands in for the expert FFN with a timing model (protocols.cpp:294-322) —
+ * with the real MoE-layer forward: gate/route -> permute -> dispatch puts +
+ * signals over NVLink -> SwiGLU expert FFN on tcgen05 -> combine puts +
+ * signals -> weighted reduce.
+ * ------------------------------------------------------------------------- */
+
+/* routing */
+#define PERSEUS_ROUTE_BALANCED 0 /* reference exact-capacity routing (workload.cpp:180-195) */
+#define PERSEUS_ROUTE_ZIPF 1     /* reference Zipf routing (workload.cpp:57-97) */
+#define PERSEUS_ROUTE_GATE 2     /* learned top-k over fp32 gate logits (new) */
+
+/* signalling (protocols.hpp:13-37 Signaling + group_size):
+ *   COUPLED   — Put, Fence, Signal per transfer tile (vanilla, protocols.cpp:242-248)
+ *   DECOUPLED — Alg. 1: puts + group counter, one fence per group, then the
+ *               group's signals (protocols.cpp:250-292); group_size 0 = per PE
+ *   NONE      — fault injection: fences suppressed (transport.cpp:104-106) */
+#define PERSEUS_SIGNAL_COUPLED 0
+#define PERSEUS_SIGNAL_DECOUPLED 1
+#define PERSEUS_SIGNAL_NONE 2
+
+typedef struct perseus_layer_config {
+    int64_t hidden_dim;       /* H  (ModelConfig, workload.hpp:16-25) */
+    int64_t intermediate_dim; /* I  */
+    int64_t experts;          /* E  */
+    int64_t top_k;            /* k  */
+    uint64_t tokens_per_pe;   /* S  (DispatchWorkload::tokens_per_pe) */
+    int32_t routing;          /* PERSEUS_ROUTE_* */
+    double skew;              /* Zipf exponent (routing == ZIPF) */
+    uint64_t seed;            /* workload seed (config.hpp:36) */
+    int32_t signaling;        /* PERSEUS_SIGNAL_* */
+    int64_t group_size;       /* DECOUPLED: 0 = one group per destination PE */
+    int32_t flags;            /* PERSEUS_F_* */
+} perseus_layer_config;
+
+#define PERSEUS_F_SYNTH_WEIGHTS 1 /* generate weights on device from `seed` */
+
+/* Tile granularity: 128 token rows per transfer tile / GEMM M-tile, i.e. the
+ * reference's tile_bytes = 128 * H * 2 (workload.hpp:58). */
+#define PERSEUS_TILE_ROWS 128
+
+typedef struct perseus_layer perseus_layer;
+
+int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, int device,
+                         perseus_layer** out);
+int perseus_layer_destroy(perseus_layer* layer);
+
+/* Symmetric-heap bootstrap (SymmetricHeap, transport.hpp:130-156): export this
+ * rank's cudaIpc handle blob, then import every rank's blob (world * len bytes,
+ * rank-major).  For ranks emulated inside ONE process on ONE device use
+ * perseus_layer_connect_local instead (raw pointers, no IPC). */
+int perseus_layer_ipc_export(perseus_layer* layer, void* blob, size_t cap, size_t* len);
+int perseus_layer_ipc_import(perseus_layer* layer, const void* blobs, size_t len_each);
+int perseus_layer_connect_local(perseus_layer* const* ranks, int world);
+
+/* Weights (device pointers, bf16 row-major): router wg[E][H]; this rank's
+ * experts e = rank + world*j: w1[E/P][2I][H] (gate rows then up rows),
+ * w2[E/P][H][I].  Copied into the handle. */
+int perseus_layer_set_weights(perseus_layer* layer, const void* wg, const void* w1,
+                              const void* w2, void* stream);
+/* Generate the synthetic bf16 tensors of the oracle's counter hash on device. */
+int perseus_layer_init_synthetic(perseus_layer* layer, uint64_t seed, void* stream);
+int perseus_fill_synthetic_x(perseus_layer* layer, void* x, uint64_t seed, void* stream);
+
+/* Forward over this rank's S tokens: x[S][H] bf16 -> out[S][H] bf16 (device
+ * pointers).  Launches asynchronously on `stream` (cudaStream_t, NULL =
+ * default).  All ranks call it; ranks synchronise through device flags only. */
+int perseus_layer_forward(perseus_layer* layer, const void* x, void* out, void* stream);
+
+/* Same, from/to HOST buffers (pinned or pageable): H2D copy, forward, D2H copy,
+ * stream-synchronised.  The end-to-end entry a reference user calls. */
+int perseus_layer_forward_host(perseus_layer* layer, const void* x_host, void* out_host,
+                               void* stream);
+
+/* Phased forward for P ranks emulated on one device: phase p of every rank
+ * must complete before phase p+1 of any rank (no cross-launch spin-waits on
+ * one GPU).  PERSEUS_PHASE_ALL == perseus_layer_forward. */
+#define PERSEUS_PHASE_ROUTE 0    /* gate/route + permutation + count publish */
+#define PERSEUS_PHASE_DISPATCH 1 /* plan + dispatch puts + signals */
+#define PERSEUS_PHASE_EXPERT 2   /* grouped SwiGLU FFN + combine puts + signals */
+#define PERSEUS_PHASE_COMBINE 3  /* weighted reduce */
+#define PERSEUS_PHASE_ALL 15
+int perseus_layer_forward_phase(perseus_layer* layer, int phase, const void* x, void* out,
+                                void* stream);
+
+/* Evidence read-back (host copies, stream-synchronised). */
+typedef struct perseus_counters {
+    int64_t epoch;                 /* forwards run */
+    int64_t dispatch_fences;       /* sys-scope fences issued, dispatch phase (this PE) */
+    int64_t dispatch_signals;      /* flag words written to peers */
+    int64_t dispatch_puts;         /* transfer tiles stored to peers */
+    int64_t dispatch_put_bytes;
+    int64_t combine_fences;
+    int64_t combine_signals;
+    int64_t combine_puts;
+    int64_t combine_put_bytes;
+    int64_t recv_tiles;            /* M-tiles processed by the expert FFN here */
+    int64_t wait_timeouts;         /* bounded spin-waits that gave up (must be 0) */
+    int64_t errors;                /* device-detected plan errors (must be 0) */
+} perseus_counters;
+int perseus_layer_counters(perseus_layer* layer, perseus_counters* out);
+
+/* Routing of the last forward: ids[S*k] int32, weights[S*k] fp32, counts[E]
+ * (this rank's per-expert token counts), positions pos[S*k] (sorted slot of
+ * each (token, j) pair).  Any pointer may be NULL. */
+int perseus_layer_read_routing(perseus_layer* layer, int32_t* ids, float* weights,
+                               int32_t* counts, int32_t* pos);
+
+/* The dispatch layout this rank realised in the last forward, as reference
+ * TransferSpecs (its remote transfer tiles with tile ids and heap offsets at
+ * the destination), and the per-destination flag words observed set at this
+ * rank.  n_* receive counts; call with NULL arrays to size. */
+int perseus_layer_read_layout(perseus_layer* layer, perseus_transfer* sent, size_t cap,
+                              size_t* n_sent, int64_t* flags_seen, size_t flags_cap,
+                              size_t* n_flags_seen);
+
+/* The count table [P][E] this rank received from all ranks in the last forward. */
+int perseus_layer_read_count_table(perseus_layer* layer, int32_t* table);
+
+/* Timing of the phases of the last forward, in ms (CUDA events). */
+int perseus_layer_read_timing(perseus_layer* layer, float* ms, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PERSEUS_H_ */

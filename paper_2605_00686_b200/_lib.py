@@ -1,0 +1,113 @@
+"""ctypes binding of libperseus.so (include/perseus.h).
+
+The product path: every call goes through the C ABI into the CUDA library.
+There is no fallback — if the library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libperseus.so")
+
+OK, ERR_CONFIG, ERR_VERIFY, ERR_RUNTIME = 0, 1, 2, 3
+ROUTE_BALANCED, ROUTE_ZIPF, ROUTE_GATE = 0, 1, 2
+SIGNAL_COUPLED, SIGNAL_DECOUPLED, SIGNAL_NONE = 0, 1, 2
+PHASE_ROUTE, PHASE_DISPATCH, PHASE_EXPERT, PHASE_COMBINE, PHASE_ALL = 0, 1, 2, 3, 15
+F_SYNTH_WEIGHTS = 1
+TILE_ROWS = 128
+
+
+class ConfigError(ValueError):
+    """sigsim::ConfigError (sim.hpp:20-22) — status 1."""
+
+
+class VerifyError(RuntimeError):
+    """verification / ordering failure — status 2."""
+
+
+class ModelError(RuntimeError):
+    """sigsim::ModelError / CUDA / timeout — status 3."""
+
+
+class Transfer(C.Structure):
+    _fields_ = [("src_pe", C.c_uint32), ("dst_pe", C.c_uint32), ("expert", C.c_int64),
+                ("bytes", C.c_uint64), ("tile_id", C.c_int64), ("heap_offset", C.c_uint64)]
+
+
+class LayerConfig(C.Structure):
+    _fields_ = [("hidden_dim", C.c_int64), ("intermediate_dim", C.c_int64),
+                ("experts", C.c_int64), ("top_k", C.c_int64), ("tokens_per_pe", C.c_uint64),
+                ("routing", C.c_int32), ("skew", C.c_double), ("seed", C.c_uint64),
+                ("signaling", C.c_int32), ("group_size", C.c_int64), ("flags", C.c_int32)]
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "epoch", "dispatch_fences", "dispatch_signals", "dispatch_puts", "dispatch_put_bytes",
+        "combine_fences", "combine_signals", "combine_puts", "combine_put_bytes", "recv_tiles",
+        "wait_timeouts", "errors")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, i64, u64, i32 = C.c_void_p, C.c_size_t, C.c_int64, C.c_uint64, C.c_int32
+    P = C.POINTER
+    sig = {
+        "perseus_last_error": (C.c_char_p, []),
+        "perseus_abi_version": (C.c_int, []),
+        "perseus_remote_transfer_count": (C.c_int, [i64, i64, i64, P(i64)]),
+        "perseus_message_size": (u64, [u64, i64, i64, i64]),
+        "perseus_zipf_route": (C.c_int, [u64, i64, C.c_double, i64, u64, P(u64), P(i32)]),
+        "perseus_build_dispatch": (C.c_int, [i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, u64,
+                                             C.c_double, u64, u64, P(Transfer), sz, P(sz),
+                                             P(Transfer), sz, P(sz), P(u64)]),
+        "perseus_assign_groups": (C.c_int, [P(Transfer), sz, i64, P(i64), P(i64), P(sz)]),
+        "perseus_heap_digest": (u64, [P(u64), sz, P(u64), sz]),
+        "perseus_fnv1a64": (u64, [vp, sz, u64]),
+        "perseus_layer_create": (C.c_int, [P(LayerConfig), C.c_int, C.c_int, C.c_int, P(vp)]),
+        "perseus_layer_destroy": (C.c_int, [vp]),
+        "perseus_layer_ipc_export": (C.c_int, [vp, vp, sz, P(sz)]),
+        "perseus_layer_ipc_import": (C.c_int, [vp, vp, sz]),
+        "perseus_layer_connect_local": (C.c_int, [P(vp), C.c_int]),
+        "perseus_layer_set_weights": (C.c_int, [vp, vp, vp, vp, vp]),
+        "perseus_layer_init_synthetic": (C.c_int, [vp, u64, vp]),
+        "perseus_fill_synthetic_x": (C.c_int, [vp, vp, u64, vp]),
+        "perseus_layer_forward": (C.c_int, [vp, vp, vp, vp]),
+        "perseus_layer_forward_host": (C.c_int, [vp, vp, vp, vp]),
+        "perseus_layer_forward_phase": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "perseus_layer_counters": (C.c_int, [vp, P(Counters)]),
+        "perseus_layer_read_routing": (C.c_int, [vp, P(i32), P(C.c_float), P(i32), P(i32)]),
+        "perseus_layer_read_layout": (C.c_int, [vp, P(Transfer), sz, P(sz), P(i64), sz, P(sz)]),
+        "perseus_layer_read_count_table": (C.c_int, [vp, P(i32)]),
+        "perseus_layer_read_timing": (C.c_int, [vp, P(C.c_float), C.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+# every symbol include/perseus.h declares (checked by the CPU tests)
+EXPORTED = [n for n in dir(lib) if n.startswith("perseus_")]
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = lib.perseus_last_error().decode(errors="replace")
+    if rc == ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == ERR_VERIFY:
+        raise VerifyError(msg)
+    raise ModelError(msg)

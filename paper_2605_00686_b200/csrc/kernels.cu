@@ -1,0 +1,643 @@
+// kernels.cu — the CUDA-core stages of the layer forward (sm_100a):
+//   synthetic tensors, gate logits (pinned fp32 order), route (top-k / reference
+//   routing + combine weights), permutation (stable counting sort), count
+//   exchange, the per-forward device plan, dispatch puts + signals, combine.
+// The grouped expert FFN (tcgen05) is in gemm.cu.
+#include <cuda_runtime.h>
+
+#include "layer_dev.h"
+#include "perseus.h"
+#include "ptx.cuh"
+
+namespace perseus {
+
+using namespace ptx;
+
+// ------------------------------------------------------------ synthetic ----
+// Same counter hash as oracle/oracle.c:orc_fill_bf16 (bit-identical bf16).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_synth_fill(bf16* __restrict__ out, uint64_t base, uint64_t first, uint64_t n,
+                             float scale) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t h = splitmix64(base + first + i);
+        const float f = __fsub_rn(__fmul_rn(float(uint32_t(h >> 40)), 0x1.0p-23f), 1.0f);
+        out[i] = __float2bfloat16_rn(__fmul_rn(f, scale));
+    }
+}
+
+void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, float scale,
+                       cudaStream_t st) {
+    if (!n) return;
+    k_synth_fill<<<148 * 8, 256, 0, st>>>(out, base, first, n, scale);
+}
+
+// ------------------------------------------------------------------ gate ----
+// logits[t][e] = sum_h x[t][h] * wg[e][h]: ONE fmaf per h, h ascending — the
+// contract oracle.c:orc_gate_logits restates, so logits (and learned top-k ids)
+// are bit-exact.  CTA tile: 64 tokens x 64 experts; thread: 8 tokens x 2 experts.
+constexpr int kGateT = 64, kGateE = 64, kGateH = 32;
+
+__global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const bf16* __restrict__ wg,
+                                              float* __restrict__ logits, int S, int H, int E) {
+    __shared__ __align__(16) float xs[kGateH][kGateT];
+    __shared__ __align__(16) float ws[kGateH][kGateE];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t0 = blockIdx.x * kGateT, e0 = blockIdx.y * kGateE;
+    float acc[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.f;
+
+    const int lr = tid >> 2, lh = (tid & 3) * 8;  // loader: row, 8-wide h chunk
+    for (int h0 = 0; h0 < H; h0 += kGateH) {
+        {
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (t0 + lr < S) v = *reinterpret_cast<const uint4*>(x + size_t(t0 + lr) * H + h0 + lh);
+            const bf16* b = reinterpret_cast<const bf16*>(&v);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) xs[lh + q][lr] = __bfloat162float(b[q]);
+            uint4 w = make_uint4(0, 0, 0, 0);
+            if (e0 + lr < E) w = *reinterpret_cast<const uint4*>(wg + size_t(e0 + lr) * H + h0 + lh);
+            const bf16* c = reinterpret_cast<const bf16*>(&w);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ws[lh + q][lr] = __bfloat162float(c[q]);
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int h = 0; h < kGateH; ++h) {
+            const float4 xa = *reinterpret_cast<const float4*>(&xs[h][warp * 8]);
+            const float4 xb = *reinterpret_cast<const float4*>(&xs[h][warp * 8 + 4]);
+            const float2 wv = *reinterpret_cast<const float2*>(&ws[h][lane * 2]);
+            const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                acc[q][0] = __fmaf_rn(xv[q], wv.x, acc[q][0]);
+                acc[q][1] = __fmaf_rn(xv[q], wv.y, acc[q][1]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int t = t0 + warp * 8 + q;
+        if (t >= S) continue;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int e = e0 + lane * 2 + i;
+            if (e < E) logits[size_t(t) * E + e] = acc[q][i];
+        }
+    }
+}
+
+// ----------------------------------------------------------------- route ----
+// One warp per token: choose k experts, then softmax over their logits.
+//   GATE     : top-k by descending logit, ties to the lower index (orc_topk)
+//   BALANCED : id[t*k+j] = (t*k+j) mod E (exact capacity, workload.cpp:180-195)
+//   ZIPF     : the reference's Zipf draws (workload.cpp:57-97), host-expanded
+__global__ void __launch_bounds__(256) k_route(DevCtx c) {
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t >= c.S) return;
+    const float* l = c.logits + size_t(t) * c.E;
+    int my_id = -1;  // lane j < k holds the j-th chosen expert
+    if (c.routing == PERSEUS_ROUTE_GATE) {
+        constexpr int kMaxPer = 32;  // E <= 1024
+        float v[kMaxPer];
+        const int per = (c.E + 31) / 32;
+#pragma unroll
+        for (int i = 0; i < kMaxPer; ++i) v[i] = (i < per && lane + 32 * i < c.E) ? l[lane + 32 * i] : -INFINITY;
+        unsigned taken = 0;  // bit i: slot i already chosen
+        for (int j = 0; j < c.k; ++j) {
+            float bv = -INFINITY;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int i = 0; i < kMaxPer; ++i) {
+                const int e = lane + 32 * i;
+                if (i < per && e < c.E && !(taken >> i & 1u) && (v[i] > bv || (v[i] == bv && e < bi))) {
+                    bv = v[i];
+                    bi = e;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+            }
+            if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+            if (lane == j) my_id = bi;
+        }
+    } else if (lane < c.k) {
+        const int64_t flat = int64_t(t) * c.k + lane;
+        my_id = c.routing == PERSEUS_ROUTE_BALANCED ? int(flat % c.E) : c.zipf_ids[flat];
+    }
+    const float mine = lane < c.k ? l[my_id] : -INFINITY;
+    float m = mine;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float ex = lane < c.k ? expf(mine - m) : 0.f;
+    float s = ex;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane < c.k) {
+        c.ids[size_t(t) * c.k + lane] = my_id;
+        c.weights[size_t(t) * c.k + lane] = ex / s;
+    }
+}
+
+// ----------------------------------------------------------- permutation ----
+__global__ void __launch_bounds__(256) k_count(DevCtx c) {
+    extern __shared__ int32_t hist[];
+    for (int e = threadIdx.x; e < c.E; e += blockDim.x) hist[e] = 0;
+    __syncthreads();
+    const int64_t n = int64_t(c.S) * c.k;
+    const int64_t i0 = int64_t(blockIdx.x) * 4096;
+    for (int64_t i = i0 + threadIdx.x; i < n && i < i0 + 4096; i += blockDim.x) atomicAdd(&hist[c.ids[i]], 1);
+    __syncthreads();
+    for (int e = threadIdx.x; e < c.E; e += blockDim.x)
+        if (hist[e]) atomicAdd(&c.counts[e], hist[e]);
+}
+
+// Stable counting-sort scatter: one CTA per expert walks the (token, j) pairs
+// in order and ranks its matches with warp ballots (orc_permute).
+__global__ void __launch_bounds__(1024) k_scatter(DevCtx c) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t s_base, s_off;
+    const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        int32_t o = 0;
+        for (int q = 0; q < e; ++q) o += c.counts[q];
+        s_off = o;
+        s_base = 0;
+        c.offsets[e] = o;
+        if (e == c.E - 1) c.offsets[c.E] = o + c.counts[e];
+    }
+    __syncthreads();
+    const int32_t off = s_off;
+    const int64_t n = int64_t(c.S) * c.k;
+    for (int64_t i0 = 0; i0 < n; i0 += 1024) {
+        const int64_t i = i0 + tid;
+        const bool m = i < n && c.ids[i] == e;
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        if (lane == 0) wsum[warp] = __popc(bal);
+        __syncthreads();
+        if (warp == 0) {
+            const int v = wsum[lane];
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            wsum[lane] = incl - v;
+        }
+        __syncthreads();
+        const int32_t base = s_base;
+        if (m) {
+            const int32_t r = off + base + wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+            c.rows[r] = int32_t(i / c.k);
+            c.pos[i] = r;
+        }
+        __syncthreads();
+        if (tid == 1023) s_base = base + wsum[31] + __popc(bal);
+        __syncthreads();
+    }
+}
+
+// -------------------------------------------------------- count exchange ----
+// Publish this rank's per-expert counts into every PE's count table (peer
+// stores), one sys-scope fence, then the per-source ready flags.
+__global__ void __launch_bounds__(256) k_publish_counts(DevCtx c) {
+    for (int p = 0; p < c.P; ++p) {
+        int32_t* dst = c.count_table[p] + (size_t(c.par) * c.P + c.rank) * c.E;
+        for (int e = threadIdx.x; e < c.E; e += blockDim.x) dst[e] = c.counts[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_acq_rel_sys();
+        for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
+    }
+}
+
+// ------------------------------------------------------------------ plan ----
+// Block-wide exclusive scan of n ints in shared memory (1024 threads).
+__device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*32*/) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + 1023) / 1024;
+    const int b = tid * per;
+    int32_t local = 0;
+    for (int i = 0; i < per; ++i)
+        if (b + i < n) local += a[b + i];
+    int32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) scratch[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int32_t v = scratch[lane];
+        int32_t wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += u;
+        }
+        scratch[lane] = wi - v;
+        if (lane == 31) scratch[32] = wi;
+    }
+    __syncthreads();
+    int32_t run = scratch[warp] + incl - local;
+    for (int i = 0; i < per; ++i)
+        if (b + i < n) {
+            const int32_t v = a[b + i];
+            a[b + i] = run;
+            run += v;
+        }
+    const int32_t total = scratch[32];
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
+
+// The per-forward layout, computed on the device from the [P][E] count table
+// every rank published.  It reproduces the reference's layout exactly:
+//   tile ids     — global counter in (src, expert, chunk) order over remote
+//                  pairs (workload.cpp:136-149, with tile_bytes = 128*H*2)
+//   heap offsets — per-destination cursor in the same order (:146-147)
+//   groups       — (dst, expert, tile) order; per-dst or fixed size
+//                  (protocols.cpp:52-94)
+__global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
+    extern __shared__ int32_t sm[];
+    const int P = c.P, E = c.E, El = c.E_loc, r = c.rank, tid = threadIdx.x;
+    const int PE = P * E;
+    int32_t* T = sm;              // [P][E] counts
+    int32_t* tb = T + PE;         // tile-id base per (s, e), s-major
+    int32_t* hr = tb + PE;        // heap row scan, (d, s, j) order
+    int32_t* off = hr + PE;       // sorted offsets per (s, e)
+    int32_t* sp = off + PE;       // send position per e (key order)
+    int32_t* rp = sp + E;         // recv position per (ks, j)
+    int32_t* scratch = rp + E;    // 33
+    __shared__ int32_t s_err;
+    __shared__ int32_t dst_first[kMaxPes + 1], dst_group[kMaxPes], src_first[kMaxPes + 1],
+        src_group[kMaxPes];
+
+    if (tid == 0) s_err = 0;
+    if (tid < P) {
+        if (!wait_flag_geq(c.count_flag[r] + tid, c.epoch, kWaitTimeoutNs)) {
+            atomicAdd(&c.stats[kStatTimeouts], 1ull);
+            s_err = 1;
+        }
+    }
+    __syncthreads();
+    const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
+    for (int i = tid; i < PE; i += 1024) {
+        const int32_t v = ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i));
+        const int s = i / E, e = i % E;
+        T[i] = v;
+        tb[i] = (s != e % P) ? ceil_tiles(v) : 0;
+        off[i] = v;
+        const int d = e % P, j = e / P;
+        hr[(d * P + s) * El + j] = (s != d) ? v : 0;
+    }
+    __syncthreads();
+    const int32_t total_tiles = block_exclusive_scan(tb, PE, scratch);
+    const int32_t total_hr = block_exclusive_scan(hr, PE, scratch);
+    // rows received here from peers: the extent of destination block r
+    const int32_t rows_in_r = (r + 1 < P ? hr[(r + 1) * P * El] : total_hr) - hr[r * P * El];
+    // per-row exclusive scans of off (sorted offsets inside each source)
+    if (tid < P) {
+        int32_t run = 0;
+        for (int e = 0; e < E; ++e) {
+            const int32_t v = off[tid * E + e];
+            off[tid * E + e] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+
+    // ---- send side (this rank as source) ----
+    // key order: remote destinations ascending, then the self segment
+    for (int e = tid; e < E; e += 1024) {
+        const int d = e % P, j = e / P;
+        const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
+        sp[kd * El + j] = ceil_tiles(T[r * E + e]);
+    }
+    __syncthreads();
+    const int32_t n_send = block_exclusive_scan(sp, E, scratch);
+    if (tid == 0) {
+        // first send position of every destination + dense per-dst group ids
+        int g = 0;
+        for (int kd = 0; kd < P; ++kd) {
+            const int d = kd < r ? kd : (kd < P - 1 ? kd + 1 : r);
+            const int first = sp[kd * El];
+            const int last = kd + 1 < P ? sp[(kd + 1) * El] : n_send;
+            dst_first[d] = first;
+            dst_group[d] = (d != r && last > first) ? g++ : -1;
+        }
+        dst_first[kMaxPes] = g;
+    }
+    __syncthreads();
+    const int32_t n_send_remote = dst_first[r];
+    const int gs = c.group_size;
+    if (gs > 0 && n_send_remote % gs != 0) s_err = 2;
+    const int32_t n_groups = gs > 0 ? n_send_remote / gs : dst_first[kMaxPes];
+
+    for (int e = tid; e < E; e += 1024) {
+        const int d = e % P, j = e / P;
+        const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
+        const int32_t cnt = T[r * E + e];
+        const int nt = ceil_tiles(cnt);
+        int32_t pos0 = sp[kd * El + j];
+        int64_t hrow;
+        if (d != r) {
+            hrow = hr[(d * P + r) * El + j] - hr[d * P * El];
+        } else {
+            int32_t so = 0;
+            for (int jj = 0; jj < j; ++jj) so += T[r * E + r + P * jj];
+            hrow = rows_in_r + so;
+        }
+        for (int ch = 0; ch < nt; ++ch) {
+            SendTile st;
+            st.expert = e;
+            st.dst = d;
+            st.row0 = ch * kTileRows;
+            st.rows = min(kTileRows, cnt - ch * kTileRows);
+            st.heap_row = hrow + int64_t(ch) * kTileRows;
+            st.tile_id = d != r ? tb[r * E + e] + ch : -1;
+            const int p = pos0 + ch;
+            st.group = d == r ? -1 : (gs > 0 ? p / gs : dst_group[d]);
+            if (p < c.max_send) c.send[p] = st; else s_err = 3;
+        }
+    }
+    // groups (dispatch direction)
+    if (gs > 0) {
+        for (int g = tid; g < n_groups; g += 1024) {
+            Group G;
+            G.first = g * gs;
+            G.count = gs;
+            G.peer = -1;
+            G.pad = 0;
+            c.groups[g] = G;
+            c.group_ctr[g] = 0;
+        }
+    } else if (tid < P && tid != r && dst_group[tid] >= 0) {
+        const int d = tid;
+        int kd = d < r ? d : d - 1;
+        const int last = kd + 1 < P ? sp[(kd + 1) * El] : n_send;
+        Group G;
+        G.peer = d;
+        G.first = dst_first[d];
+        G.count = last - dst_first[d];
+        G.pad = 0;
+        c.groups[dst_group[d]] = G;
+        c.group_ctr[dst_group[d]] = 0;
+    }
+
+    // ---- receive side (this rank as destination) ----
+    for (int i = tid; i < P * El; i += 1024) {
+        const int s = i / El, j = i % El;
+        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+        rp[ks * El + j] = ceil_tiles(T[s * E + r + P * j]);
+    }
+    __syncthreads();
+    const int32_t n_recv = block_exclusive_scan(rp, P * El, scratch);
+    if (tid == 0) {
+        int g = 0;
+        for (int ks = 0; ks < P; ++ks) {
+            const int s = ks == 0 ? r : (ks <= r ? ks - 1 : ks);
+            const int first = rp[ks * El];
+            const int last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
+            src_first[s] = first;
+            src_group[s] = (s != r && last > first) ? g++ : -1;
+        }
+    }
+    __syncthreads();
+    const int32_t n_recv_self = (P > 1) ? rp[El] : n_recv;
+    const int32_t n_recv_remote = n_recv - n_recv_self;
+    if (gs > 0 && n_recv_remote % gs != 0) s_err = 4;
+    int32_t n_cgroups = 0;
+    if (gs > 0) n_cgroups = n_recv_remote / gs;
+    else for (int s = 0; s < P; ++s) n_cgroups += src_group[s] >= 0;
+
+    for (int i = tid; i < P * El; i += 1024) {
+        const int s = i / El, j = i % El, e = r + P * j;
+        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+        const int32_t cnt = T[s * E + e];
+        const int nt = ceil_tiles(cnt);
+        const int32_t pos0 = rp[ks * El + j];
+        int64_t hrow;
+        if (s != r) {
+            hrow = hr[(r * P + s) * El + j] - hr[r * P * El];
+        } else {
+            int32_t so = 0;
+            for (int jj = 0; jj < j; ++jj) so += T[r * E + r + P * jj];
+            hrow = rows_in_r + so;
+        }
+        for (int ch = 0; ch < nt; ++ch) {
+            RecvTile rt;
+            rt.src = s;
+            rt.e_local = j;
+            rt.rows = min(kTileRows, cnt - ch * kTileRows);
+            rt.tile_id = s != r ? tb[s * E + e] + ch : -1;
+            rt.heap_row = hrow + int64_t(ch) * kTileRows;
+            rt.ybuf_row = off[s * E + e] + int64_t(ch) * kTileRows;
+            const int p = pos0 + ch;
+            rt.cgroup = s == r ? -1 : (gs > 0 ? (p - n_recv_self) / gs : src_group[s]);
+            rt.pad = 0;
+            if (p < c.max_recv) {
+                c.recv[p] = rt;
+                c.tile_ctr[p] = 0;
+            } else {
+                s_err = 5;
+            }
+        }
+    }
+    if (gs > 0) {
+        for (int g = tid; g < n_cgroups; g += 1024) {
+            Group G;
+            G.first = n_recv_self + g * gs;
+            G.count = gs;
+            G.peer = -1;
+            G.pad = 0;
+            c.cgroups[g] = G;
+            c.cgroup_ctr[g] = 0;
+        }
+    } else if (tid < P && tid != r && src_group[tid] >= 0) {
+        const int s = tid;
+        const int ks = s < r ? s + 1 : s;
+        const int last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
+        Group G;
+        G.peer = s;
+        G.first = src_first[s];
+        G.count = last - src_first[s];
+        G.pad = 0;
+        c.cgroups[src_group[s]] = G;
+        c.cgroup_ctr[src_group[s]] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        PlanHeader h;
+        h.n_send = n_send;
+        h.n_send_remote = n_send_remote;
+        h.n_groups = n_groups;
+        h.n_recv = n_recv;
+        h.n_recv_remote = n_recv_remote;
+        h.n_cgroups = n_cgroups;
+        h.total_tiles = total_tiles;
+        h.error = s_err;
+        h.remote_rows_in = rows_in_r;
+        *c.hdr = h;
+        if (s_err) atomicAdd(&c.stats[kStatErrors], 1ull);
+    }
+}
+
+// ---------------------------------------------------------- signalling ----
+// Phase 2 of Alg. 1 for one group, executed by the thread that completed the
+// group's counter: ONE sys-scope fence, then every member's flag word in
+// member order (protocols.cpp:275-292).  With suppress (fault injection) the
+// fence is dropped (transport.cpp:104-106).
+template <class FlagOf>
+__device__ void signal_group(const DevCtx& c, const Group& g, FlagOf flag_of, bool suppress,
+                             int stat_fence, int stat_signal) {
+    if (!suppress) {
+        fence_acq_rel_sys();
+        atomicAdd(&c.stats[stat_fence], 1ull);
+    }
+    for (int m = 0; m < g.count; ++m) st_relaxed_sys(flag_of(g.first + m), c.epoch);
+    atomicAdd(&c.stats[stat_signal], (unsigned long long)g.count);
+}
+
+// -------------------------------------------------------------- dispatch ----
+// One CTA per send tile: gather the tile's token rows (sorted order) and store
+// them into the destination's receive heap — a one-sided NVLink store for a
+// peer, a local copy for the self segment — then signal (Phase 1: counter;
+// the completing producer runs Phase 2).
+__global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
+    const PlanHeader hdr = *c.hdr;
+    const int i = blockIdx.x;
+    if (i >= hdr.n_send || hdr.error) return;
+    const SendTile st = c.send[i];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t abs0 = c.offsets[st.expert] + st.row0;
+    bf16* dbase = c.heap[st.dst] + (size_t(c.par) * c.R_max + st.heap_row) * c.H;
+    const int nvec = c.H / 8;  // 16-byte vectors per row
+    for (int rr = warp; rr < st.rows; rr += 8) {
+        const int32_t tok = c.rows[abs0 + rr];
+        const uint4* src = reinterpret_cast<const uint4*>(c.x + size_t(tok) * c.H);
+        uint4* dst = reinterpret_cast<uint4*>(dbase + size_t(rr) * c.H);
+        int v = lane;
+        for (; v + 96 < nvec; v += 128) {
+            const uint4 a = __ldg(src + v), b = __ldg(src + v + 32), d = __ldg(src + v + 64),
+                        e = __ldg(src + v + 96);
+            dst[v] = a;
+            dst[v + 32] = b;
+            dst[v + 64] = d;
+            dst[v + 96] = e;
+        }
+        for (; v < nvec; v += 32) dst[v] = __ldg(src + v);
+    }
+    if (st.dst == c.rank) return;  // self segment: ordered by the stream, no signal
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
+    atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
+    const bool suppress = c.signaling == PERSEUS_SIGNAL_NONE;
+    const Group g = c.groups[st.group];
+    auto flag_of = [&](int m) {
+        const SendTile& t = c.send[m];
+        return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
+    };
+    if (g.count == 1) {
+        signal_group(c, g, flag_of, suppress, kStatDispatchFences, kStatDispatchSignals);
+    } else {
+        // Phase 1: publish this tile into the group counter (gpu-scope
+        // release covers the CTA's stores via the barrier above).
+        const uint32_t old = atom_add_acq_rel_gpu(c.group_ctr + st.group, 1u);
+        if (old + 1 == uint32_t(g.count))
+            signal_group(c, g, flag_of, suppress, kStatDispatchFences, kStatDispatchSignals);
+    }
+}
+
+// --------------------------------------------------------------- combine ----
+// Wait for every combine tile this rank dispatched to come back, then
+// out[t] = sum_j w[t][j] * y[pos(t, j)] in fixed j order (fp32) -> bf16.
+__global__ void __launch_bounds__(256) k_combine(DevCtx c) {
+    const PlanHeader hdr = *c.hdr;
+    if (c.P > 1 && threadIdx.x < 32) {
+        const uint32_t* flags = c.cflag[c.rank] + size_t(c.par) * c.T_max;
+        for (int q = threadIdx.x; q < hdr.n_send_remote; q += 32) {
+            const int tile = c.send[q].tile_id;
+            if (!wait_flag_geq(flags + tile, c.epoch, kWaitTimeoutNs))
+                atomicAdd(&c.stats[kStatTimeouts], 1ull);
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t >= c.S) return;
+    const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
+    int32_t p[16];
+    float w[16];
+    for (int j = 0; j < c.k; ++j) {
+        p[j] = c.pos[size_t(t) * c.k + j];
+        w[j] = c.weights[size_t(t) * c.k + j];
+    }
+    const int nvec = c.H / 8;
+    for (int v = lane; v < nvec; v += 32) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = 0; j < c.k; ++j) {
+            const uint4 u = *reinterpret_cast<const uint4*>(y + size_t(p[j]) * c.H + v * 8);
+            const bf16* b = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = __fmaf_rn(w[j], __bfloat162float(b[q]), acc[q]);
+        }
+        uint4 o;
+        o.x = pack_bf16(acc[0], acc[1]);
+        o.y = pack_bf16(acc[2], acc[3]);
+        o.z = pack_bf16(acc[4], acc[5]);
+        o.w = pack_bf16(acc[6], acc[7]);
+        *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + v * 8) = o;
+    }
+}
+
+// ------------------------------------------------------------- launchers ----
+void launch_route(const DevCtx& c, cudaStream_t st) {
+    dim3 g((c.S + kGateT - 1) / kGateT, (c.E + kGateE - 1) / kGateE);
+    k_gate<<<g, 256, 0, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
+    k_route<<<(c.S + 7) / 8, 256, 0, st>>>(c);
+    cudaMemsetAsync(c.counts, 0, sizeof(int32_t) * c.E, st);
+    const int64_t n = int64_t(c.S) * c.k;
+    k_count<<<int((n + 4095) / 4096), 256, sizeof(int32_t) * c.E, st>>>(c);
+    k_scatter<<<c.E, 1024, 0, st>>>(c);
+    k_publish_counts<<<1, 256, 0, st>>>(c);
+}
+
+size_t plan_smem_bytes(const DevCtx& c) {
+    const size_t PE = size_t(c.P) * c.E;
+    return sizeof(int32_t) * (4 * PE + 2 * size_t(c.E) + 40);
+}
+
+void launch_dispatch(const DevCtx& c, cudaStream_t st) {
+    k_plan<<<1, 1024, plan_smem_bytes(c), st>>>(c);
+    k_dispatch<<<c.max_send, 256, 0, st>>>(c);
+}
+
+void launch_combine(const DevCtx& c, cudaStream_t st) {
+    k_combine<<<(c.S + 7) / 8, 256, 0, st>>>(c);
+}
+
+cudaError_t configure_kernels(const DevCtx& c) {
+    return cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(plan_smem_bytes(c)));
+}
+
+}  // namespace perseus

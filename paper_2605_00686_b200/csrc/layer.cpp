@@ -1,0 +1,506 @@
+// layer.cpp — host runtime of one layer rank (the C ABI of include/perseus.h).
+//
+// Owns: weights, the symmetric region (count table, receive heap, combine
+// buffer, flag words — double-buffered by forward parity), the peer mappings
+// (cudaIpc), the device plan buffers, TMA descriptors and the launch sequence.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "layer_dev.h"
+#include "perseus.h"
+#include "perseus_internal.h"
+#include "sigsim/workload.hpp"
+
+namespace perseus {
+
+// kernels.cu / gemm.cu
+void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, float scale, cudaStream_t st);
+void launch_route(const DevCtx& c, cudaStream_t st);
+void launch_dispatch(const DevCtx& c, cudaStream_t st);
+void launch_combine(const DevCtx& c, cudaStream_t st);
+cudaError_t configure_kernels(const DevCtx& c);
+size_t gemm_smem_bytes();
+cudaError_t configure_gemm();
+void launch_gemm(int mode, const CUtensorMap& ta, const CUtensorMap& tb, const DevCtx& c, int n_nb,
+                 int num_kb, int64_t a_row_base, int grid, cudaStream_t st);
+
+namespace {
+thread_local std::string g_err;
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+uint64_t splitmix64(uint64_t z) { return sigsim::SeededRng::mix(z); }
+uint64_t tensor_base(uint64_t seed, uint32_t tensor) {
+    return splitmix64(seed ^ (uint64_t(tensor) * 0xD1B54A32D192ED03ULL));
+}
+enum : uint32_t { kTX = 1, kTWG = 2, kTW1 = 3, kTW2 = 4 };
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+           "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!p || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+// bf16 row-major [rows][cols] viewed as a 2D tensor, box 64 (K) x 128 rows, SW128
+CUtensorMap make_tmap(const void* base, uint64_t rows, uint64_t cols) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace perseus
+
+using namespace perseus;
+
+struct perseus_layer {
+    perseus_layer_config cfg{};
+    int rank = 0, world = 1, device = 0;
+    int H = 0, I = 0, E = 0, k = 0, S = 0, El = 0;
+    int64_t R_max = 0, T_max = 0, Y_rows = 0;
+    int max_send = 0, max_recv = 0;
+    int num_sms = 148;
+    uint32_t epoch = 0;
+    cudaStream_t stream = nullptr;
+
+    // local
+    bf16 *x_stage = nullptr, *out_stage = nullptr;
+    bf16 *wg = nullptr, *w1 = nullptr, *w2 = nullptr, *hbuf = nullptr;
+    float *logits = nullptr, *weights = nullptr;
+    int32_t *ids = nullptr, *counts = nullptr, *offsets = nullptr, *rows = nullptr, *pos = nullptr,
+            *zipf_ids = nullptr;
+    PlanHeader* hdr = nullptr;
+    SendTile* send = nullptr;
+    Group *groups = nullptr, *cgroups = nullptr;
+    RecvTile* recv = nullptr;
+    uint32_t *group_ctr = nullptr, *cgroup_ctr = nullptr, *tile_ctr = nullptr;
+    unsigned long long* stats = nullptr;
+
+    // symmetric region
+    uint8_t* sym = nullptr;
+    size_t sym_bytes = 0;
+    size_t off_ctab = 0, off_cflag_cnt = 0, off_dflag = 0, off_cflag = 0, off_heap = 0, off_ybuf = 0;
+    uint8_t* peer[kMaxPes] = {};
+    bool ipc_mapped[kMaxPes] = {};
+    bool connected = false;
+
+    CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{};
+    cudaEvent_t ev[5] = {};
+    const void* last_x = nullptr;
+
+    DevCtx ctx(const void* x, void* out) const {
+        DevCtx c{};
+        c.H = H; c.I = I; c.E = E; c.k = k; c.P = world; c.rank = rank; c.E_loc = El; c.S = S;
+        c.routing = cfg.routing;
+        c.signaling = cfg.signaling;
+        c.group_size = cfg.signaling == PERSEUS_SIGNAL_DECOUPLED ? int32_t(cfg.group_size) : 1;
+        c.epoch = epoch;
+        c.par = int32_t(epoch & 1u);
+        c.x = static_cast<const bf16*>(x);
+        c.out = static_cast<bf16*>(out);
+        c.wg = wg; c.logits = logits; c.ids = ids; c.weights = weights; c.counts = counts;
+        c.offsets = offsets; c.rows = rows; c.pos = pos; c.zipf_ids = zipf_ids; c.hbuf = hbuf;
+        for (int p = 0; p < world; ++p) {
+            uint8_t* b = peer[p];
+            c.count_table[p] = reinterpret_cast<int32_t*>(b + off_ctab);
+            c.count_flag[p] = reinterpret_cast<uint32_t*>(b + off_cflag_cnt);
+            c.heap[p] = reinterpret_cast<bf16*>(b + off_heap);
+            c.dflag[p] = reinterpret_cast<uint32_t*>(b + off_dflag);
+            c.ybuf[p] = reinterpret_cast<bf16*>(b + off_ybuf);
+            c.cflag[p] = reinterpret_cast<uint32_t*>(b + off_cflag);
+        }
+        c.R_max = R_max; c.T_max = T_max; c.Y_rows = Y_rows;
+        c.hdr = hdr; c.send = send; c.groups = groups; c.recv = recv; c.cgroups = cgroups;
+        c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
+        c.max_send = max_send; c.max_recv = max_recv;
+        c.stats = stats;
+        return c;
+    }
+};
+
+namespace {
+
+void validate(const perseus_layer_config& c, int rank, int world) {
+    sigsim::ModelConfig m{"layer", c.hidden_dim, c.intermediate_dim, c.experts, c.top_k, 0.0};
+    m.validate();
+    if (world < 1 || world > kMaxPes) throw sigsim::ConfigError("world size must be in [1, 8]");
+    if (rank < 0 || rank >= world) throw sigsim::ConfigError("rank out of range");
+    if (c.experts % world) throw sigsim::ConfigError("experts not divisible by PEs");
+    if (c.hidden_dim % 256) throw sigsim::ConfigError("hidden_dim must be a multiple of 256");
+    if (c.intermediate_dim % 128) throw sigsim::ConfigError("intermediate_dim must be a multiple of 128");
+    if (c.experts > 1024) throw sigsim::ConfigError("experts must be <= 1024");
+    if (c.top_k > 16) throw sigsim::ConfigError("top_k must be <= 16");
+    if (int64_t(world) * c.experts > 4096) throw sigsim::ConfigError("P*E must be <= 4096");
+    if (c.tokens_per_pe == 0) throw sigsim::ConfigError("tokens_per_pe must be > 0");
+    if (c.routing == PERSEUS_ROUTE_BALANCED && (c.tokens_per_pe * uint64_t(c.top_k)) % uint64_t(c.experts))
+        throw sigsim::ConfigError("build_dispatch: balanced routing needs E | S*k");
+    if (c.routing < 0 || c.routing > 2) throw sigsim::ConfigError("unknown routing mode");
+    if (c.routing == PERSEUS_ROUTE_ZIPF && c.skew < 0.0) throw sigsim::ConfigError("zipf_route: exponent must be >= 0");
+    if (c.signaling < 0 || c.signaling > 2) throw sigsim::ConfigError("unknown signaling mode");
+    if (c.group_size < 0) throw sigsim::ConfigError("group size must be >= 0");
+}
+
+template <class T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    ck(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), "cudaMemset");
+    return static_cast<T*>(p);
+}
+
+void free_layer(perseus_layer* L) {
+    if (!L) return;
+    cudaSetDevice(L->device);
+    cudaDeviceSynchronize();
+    for (int p = 0; p < kMaxPes; ++p)
+        if (L->ipc_mapped[p]) cudaIpcCloseMemHandle(L->peer[p]);
+    void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
+                    L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hdr, L->send, L->groups,
+                    L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (auto& e : L->ev)
+        if (e) cudaEventDestroy(e);
+    if (L->stream) cudaStreamDestroy(L->stream);
+    delete L;
+}
+
+void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream_t st) {
+    if (!L->connected) throw sigsim::ModelError("layer not connected (ipc_import / connect_local)");
+    ck(cudaSetDevice(L->device), "cudaSetDevice");
+    if (phase == PERSEUS_PHASE_ROUTE || phase == PERSEUS_PHASE_ALL) ++L->epoch;
+    if (x) L->last_x = x;
+    DevCtx c = L->ctx(x ? x : L->last_x, out);
+    const bool all = phase == PERSEUS_PHASE_ALL;
+    if (all) ck(cudaEventRecord(L->ev[0], st), "event");
+    if (all || phase == PERSEUS_PHASE_ROUTE) launch_route(c, st);
+    if (all) ck(cudaEventRecord(L->ev[1], st), "event");
+    if (all || phase == PERSEUS_PHASE_DISPATCH) launch_dispatch(c, st);
+    if (all) ck(cudaEventRecord(L->ev[2], st), "event");
+    if (all || phase == PERSEUS_PHASE_EXPERT) {
+        launch_gemm(1, L->tm_a1, L->tm_b1, c, L->I / 128, L->H / 64, int64_t(c.par) * L->R_max, L->num_sms, st);
+        launch_gemm(2, L->tm_a2, L->tm_b2, c, L->H / 256, L->I / 64, 0, L->num_sms, st);
+    }
+    if (all) ck(cudaEventRecord(L->ev[3], st), "event");
+    if (all || phase == PERSEUS_PHASE_COMBINE) launch_combine(c, st);
+    if (all) ck(cudaEventRecord(L->ev[4], st), "event");
+    ck(cudaGetLastError(), "kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* perseus_last_error(void) { return perseus::g_err.c_str(); }
+
+int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, int device,
+                         perseus_layer** out) {
+    return guarded([&] {
+        *out = nullptr;
+        validate(*cfg, rank, world);
+        auto* L = new perseus_layer;
+        try {
+            L->cfg = *cfg;
+            L->rank = rank;
+            L->world = world;
+            L->device = device;
+            L->H = int(cfg->hidden_dim);
+            L->I = int(cfg->intermediate_dim);
+            L->E = int(cfg->experts);
+            L->k = int(cfg->top_k);
+            L->S = int(cfg->tokens_per_pe);
+            L->El = L->E / world;
+            const int64_t Sk = int64_t(L->S) * L->k;
+            L->R_max = int64_t(world) * L->S * std::min(L->k, L->El) + 2 * kTileRows;
+            L->T_max = int64_t(world) * (Sk / kTileRows + L->E + 1) + 16;
+            L->Y_rows = Sk + kTileRows;
+            L->max_send = int(Sk / kTileRows + L->E + 1);
+            L->max_recv = int(int64_t(world) * (int64_t(L->S) * std::min(L->k, L->El) / kTileRows + L->El + 1));
+            ck(cudaSetDevice(device), "cudaSetDevice");
+            ck(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+            ck(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
+            for (auto& e : L->ev) ck(cudaEventCreate(&e), "event");
+
+            const size_t H = L->H, I = L->I, E = L->E, El = L->El, S = L->S, P = world;
+            L->x_stage = dalloc<bf16>(S * H);
+            L->out_stage = dalloc<bf16>(S * H);
+            L->wg = dalloc<bf16>(E * H);
+            L->w1 = dalloc<bf16>(El * 2 * I * H);
+            L->w2 = dalloc<bf16>(El * H * I);
+            L->hbuf = dalloc<bf16>(size_t(L->R_max) * I);
+            L->logits = dalloc<float>(S * E);
+            L->weights = dalloc<float>(Sk);
+            L->ids = dalloc<int32_t>(Sk);
+            L->counts = dalloc<int32_t>(E);
+            L->offsets = dalloc<int32_t>(E + 1);
+            L->rows = dalloc<int32_t>(Sk);
+            L->pos = dalloc<int32_t>(Sk);
+            L->zipf_ids = dalloc<int32_t>(Sk);
+            L->hdr = dalloc<PlanHeader>(1);
+            L->send = dalloc<SendTile>(L->max_send);
+            L->groups = dalloc<Group>(L->max_send);
+            L->recv = dalloc<RecvTile>(L->max_recv);
+            L->cgroups = dalloc<Group>(L->max_recv);
+            L->group_ctr = dalloc<uint32_t>(L->max_send);
+            L->cgroup_ctr = dalloc<uint32_t>(L->max_recv);
+            L->tile_ctr = dalloc<uint32_t>(L->max_recv);
+            L->stats = dalloc<unsigned long long>(kStatCount);
+
+            // symmetric region: identical layout on every rank
+            size_t o = 0;
+            L->off_ctab = o; o = align_up(o + 2 * P * E * 4, 256);
+            L->off_cflag_cnt = o; o = align_up(o + kMaxPes * 4, 256);
+            L->off_dflag = o; o = align_up(o + 2 * size_t(L->T_max) * 4, 256);
+            L->off_cflag = o; o = align_up(o + 2 * size_t(L->T_max) * 4, 1024);
+            L->off_heap = o; o = align_up(o + 2 * size_t(L->R_max) * H * 2, 1024);
+            L->off_ybuf = o; o = align_up(o + 2 * size_t(L->Y_rows) * H * 2, 1024);
+            L->sym_bytes = o;
+            L->sym = dalloc<uint8_t>(o);
+
+            if (cfg->routing == PERSEUS_ROUTE_ZIPF) {
+                std::vector<int32_t> z;
+                sigsim::zipf_route_ids(S, L->E, cfg->skew, L->k,
+                                       cfg->seed ^ (0x9E3779B97F4A7C15ULL * uint64_t(rank + 1)), &z);
+                ck(cudaMemcpy(L->zipf_ids, z.data(), z.size() * 4, cudaMemcpyHostToDevice), "memcpy");
+            }
+            L->tm_a1 = make_tmap(L->sym + L->off_heap, 2 * uint64_t(L->R_max), H);
+            L->tm_b1 = make_tmap(L->w1, El * 2 * I, H);
+            L->tm_a2 = make_tmap(L->hbuf, uint64_t(L->R_max), I);
+            L->tm_b2 = make_tmap(L->w2, El * H, I);
+            ck(configure_gemm(), "configure_gemm");
+            ck(configure_kernels(L->ctx(nullptr, nullptr)), "configure_kernels");
+            if (world == 1) {
+                L->peer[0] = L->sym;
+                L->connected = true;
+            }
+            if (cfg->flags & PERSEUS_F_SYNTH_WEIGHTS) {
+                if (perseus_layer_init_synthetic(L, cfg->seed, nullptr)) throw CudaError(perseus::g_err);
+            }
+            ck(cudaDeviceSynchronize(), "create sync");
+        } catch (...) {
+            free_layer(L);
+            throw;
+        }
+        *out = L;
+    });
+}
+
+int perseus_layer_destroy(perseus_layer* L) {
+    return guarded([&] { free_layer(L); });
+}
+
+int perseus_layer_ipc_export(perseus_layer* L, void* blob, size_t cap, size_t* len) {
+    return guarded([&] {
+        *len = sizeof(cudaIpcMemHandle_t);
+        if (!blob) return;
+        if (cap < sizeof(cudaIpcMemHandle_t)) throw sigsim::ConfigError("ipc blob buffer too small");
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, L->sym), "cudaIpcGetMemHandle");
+        std::memcpy(blob, &h, sizeof h);
+    });
+}
+
+int perseus_layer_ipc_import(perseus_layer* L, const void* blobs, size_t len_each) {
+    return guarded([&] {
+        if (len_each != sizeof(cudaIpcMemHandle_t)) throw sigsim::ConfigError("bad ipc blob size");
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        for (int p = 0; p < L->world; ++p) {
+            if (p == L->rank) {
+                L->peer[p] = L->sym;
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const uint8_t*>(blobs) + p * len_each, sizeof h);
+            void* ptr = nullptr;
+            ck(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            L->peer[p] = static_cast<uint8_t*>(ptr);
+            L->ipc_mapped[p] = true;
+        }
+        L->connected = true;
+    });
+}
+
+int perseus_layer_connect_local(perseus_layer* const* ranks, int world) {
+    return guarded([&] {
+        for (int r = 0; r < world; ++r) {
+            if (ranks[r]->world != world || ranks[r]->rank != r) throw sigsim::ConfigError("rank list mismatch");
+            for (int p = 0; p < world; ++p) ranks[r]->peer[p] = ranks[p]->sym;
+            ranks[r]->connected = true;
+        }
+    });
+}
+
+int perseus_layer_set_weights(perseus_layer* L, const void* wg, const void* w1, const void* w2, void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        auto st = static_cast<cudaStream_t>(stream);
+        const size_t H = L->H, I = L->I, E = L->E, El = L->El;
+        if (wg) ck(cudaMemcpyAsync(L->wg, wg, E * H * 2, cudaMemcpyDeviceToDevice, st), "memcpy wg");
+        if (w1) ck(cudaMemcpyAsync(L->w1, w1, El * 2 * I * H * 2, cudaMemcpyDeviceToDevice, st), "memcpy w1");
+        if (w2) ck(cudaMemcpyAsync(L->w2, w2, El * H * I * 2, cudaMemcpyDeviceToDevice, st), "memcpy w2");
+    });
+}
+
+int perseus_layer_init_synthetic(perseus_layer* L, uint64_t seed, void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        auto st = static_cast<cudaStream_t>(stream);
+        const uint64_t H = L->H, I = L->I, E = L->E;
+        const float s_h = float(std::sqrt(3.0 / double(H))), s_i = float(std::sqrt(3.0 / double(I)));
+        launch_synth_fill(L->wg, tensor_base(seed, kTWG), 0, E * H, s_h, st);
+        for (int j = 0; j < L->El; ++j) {
+            const uint64_t e = uint64_t(L->rank) + uint64_t(L->world) * j;
+            launch_synth_fill(L->w1 + j * 2 * I * H, tensor_base(seed, kTW1), e * 2 * I * H, 2 * I * H, s_h, st);
+            launch_synth_fill(L->w2 + j * H * I, tensor_base(seed, kTW2), e * H * I, H * I, s_i, st);
+        }
+        ck(cudaGetLastError(), "synth fill");
+    });
+}
+
+int perseus_fill_synthetic_x(perseus_layer* L, void* x, uint64_t seed, void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        const uint64_t n = uint64_t(L->S) * L->H;
+        launch_synth_fill(static_cast<bf16*>(x), tensor_base(seed, kTX), uint64_t(L->rank) * n, n,
+                          float(std::sqrt(3.0)), static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "synth fill x");
+    });
+}
+
+int perseus_layer_forward(perseus_layer* L, const void* x, void* out, void* stream) {
+    return guarded([&] { run_phase(L, PERSEUS_PHASE_ALL, x, out, static_cast<cudaStream_t>(stream)); });
+}
+
+int perseus_layer_forward_phase(perseus_layer* L, int phase, const void* x, void* out, void* stream) {
+    return guarded([&] {
+        if (phase < 0 || (phase > 3 && phase != PERSEUS_PHASE_ALL)) throw sigsim::ConfigError("bad phase");
+        run_phase(L, phase, x, out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int perseus_layer_forward_host(perseus_layer* L, const void* x_host, void* out_host, void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        auto st = stream ? static_cast<cudaStream_t>(stream) : L->stream;
+        const size_t bytes = size_t(L->S) * L->H * 2;
+        ck(cudaMemcpyAsync(L->x_stage, x_host, bytes, cudaMemcpyHostToDevice, st), "H2D x");
+        run_phase(L, PERSEUS_PHASE_ALL, L->x_stage, L->out_stage, st);
+        ck(cudaMemcpyAsync(out_host, L->out_stage, bytes, cudaMemcpyDeviceToHost, st), "D2H out");
+        ck(cudaStreamSynchronize(st), "forward_host sync");
+    });
+}
+
+int perseus_layer_counters(perseus_layer* L, perseus_counters* out) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        unsigned long long s[kStatCount];
+        ck(cudaMemcpy(s, L->stats, sizeof s, cudaMemcpyDeviceToHost), "memcpy stats");
+        out->epoch = L->epoch;
+        out->dispatch_fences = int64_t(s[kStatDispatchFences]);
+        out->dispatch_signals = int64_t(s[kStatDispatchSignals]);
+        out->dispatch_puts = int64_t(s[kStatDispatchPuts]);
+        out->dispatch_put_bytes = int64_t(s[kStatDispatchBytes]);
+        out->combine_fences = int64_t(s[kStatCombineFences]);
+        out->combine_signals = int64_t(s[kStatCombineSignals]);
+        out->combine_puts = int64_t(s[kStatCombinePuts]);
+        out->combine_put_bytes = int64_t(s[kStatCombineBytes]);
+        out->recv_tiles = int64_t(s[kStatRecvTiles]);
+        out->wait_timeouts = int64_t(s[kStatTimeouts]);
+        out->errors = int64_t(s[kStatErrors]);
+    });
+}
+
+int perseus_layer_read_routing(perseus_layer* L, int32_t* ids, float* weights, int32_t* counts, int32_t* pos) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        const size_t Sk = size_t(L->S) * L->k;
+        if (ids) ck(cudaMemcpy(ids, L->ids, Sk * 4, cudaMemcpyDeviceToHost), "memcpy");
+        if (weights) ck(cudaMemcpy(weights, L->weights, Sk * 4, cudaMemcpyDeviceToHost), "memcpy");
+        if (counts) ck(cudaMemcpy(counts, L->counts, size_t(L->E) * 4, cudaMemcpyDeviceToHost), "memcpy");
+        if (pos) ck(cudaMemcpy(pos, L->pos, Sk * 4, cudaMemcpyDeviceToHost), "memcpy");
+    });
+}
+
+int perseus_layer_read_layout(perseus_layer* L, perseus_transfer* sent, size_t cap, size_t* n_sent,
+                              int64_t* flags_seen, size_t flags_cap, size_t* n_flags_seen) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        PlanHeader h;
+        ck(cudaMemcpy(&h, L->hdr, sizeof h, cudaMemcpyDeviceToHost), "memcpy hdr");
+        if (h.error) throw VerifyError("device plan error " + std::to_string(h.error));
+        std::vector<SendTile> st(size_t(std::max(h.n_send_remote, 0)));
+        if (!st.empty())
+            ck(cudaMemcpy(st.data(), L->send, st.size() * sizeof(SendTile), cudaMemcpyDeviceToHost), "memcpy send");
+        *n_sent = st.size();
+        if (sent)
+            for (size_t i = 0; i < st.size() && i < cap; ++i)
+                sent[i] = perseus_transfer{uint32_t(L->rank), uint32_t(st[i].dst), st[i].expert,
+                                           uint64_t(st[i].rows) * L->H * 2, st[i].tile_id,
+                                           uint64_t(st[i].heap_row) * L->H * 2};
+        const int par = int(L->epoch & 1u);
+        std::vector<uint32_t> fl(size_t(L->T_max));
+        ck(cudaMemcpy(fl.data(), L->sym + L->off_dflag + size_t(par) * L->T_max * 4, fl.size() * 4,
+                      cudaMemcpyDeviceToHost),
+           "memcpy flags");
+        size_t n = 0;
+        for (size_t t = 0; t < fl.size(); ++t)
+            if (fl[t] == L->epoch) {
+                if (flags_seen && n < flags_cap) flags_seen[n] = int64_t(t);
+                ++n;
+            }
+        *n_flags_seen = n;
+    });
+}
+
+int perseus_layer_read_count_table(perseus_layer* L, int32_t* table) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        const int par = int(L->epoch & 1u);
+        const size_t n = size_t(L->world) * L->E;
+        ck(cudaMemcpy(table, L->sym + L->off_ctab + size_t(par) * n * 4, n * 4, cudaMemcpyDeviceToHost), "memcpy");
+    });
+}
+
+int perseus_layer_read_timing(perseus_layer* L, float* ms, int n) {
+    return guarded([&] {
+        ck(cudaEventSynchronize(L->ev[4]), "event sync");
+        for (int i = 0; i < n && i < 4; ++i) ck(cudaEventElapsedTime(&ms[i], L->ev[i], L->ev[i + 1]), "elapsed");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+// layer_dev.h — the by-value kernel context of one layer rank.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+
+#include "perseus_internal.h"
+
+namespace perseus {
+
+using bf16 = __nv_bfloat16;
+
+struct DevCtx {
+    // geometry
+    int32_t H, I, E, k, P, rank, E_loc;
+    int32_t S;
+    int32_t routing;     // PERSEUS_ROUTE_*
+    int32_t signaling;   // PERSEUS_SIGNAL_*
+    int32_t group_size;  // effective: 1 = per tile, 0 = per destination, >1 fixed
+    uint32_t epoch;      // forward counter, value of every flag written this forward
+    int32_t par;         // epoch & 1: which half of every symmetric double buffer
+
+    // local buffers
+    const bf16* x;
+    bf16* out;
+    const bf16* wg;      // [E][H]
+    float* logits;       // [S][E]
+    int32_t* ids;        // [S][k]
+    float* weights;      // [S][k]
+    int32_t* counts;     // [E]
+    int32_t* offsets;    // [E+1]: sorted segment starts of this rank's (token, j) pairs
+    int32_t* rows;       // [S*k]: token of each sorted slot
+    int32_t* pos;        // [S*k]: sorted slot of each (token, j)
+    const int32_t* zipf_ids;  // [S*k]: reference Zipf draws (routing == ZIPF)
+    bf16* hbuf;          // [R_max][I]
+
+    // symmetric buffers, one base pointer per PE (peer-mapped; [rank] = local)
+    int32_t* count_table[kMaxPes];  // [2][P][E]
+    uint32_t* count_flag[kMaxPes];  // [P]
+    bf16* heap[kMaxPes];            // [2][R_max][H]
+    uint32_t* dflag[kMaxPes];       // [2][T_max]
+    bf16* ybuf[kMaxPes];            // [2][Y_rows][H]
+    uint32_t* cflag[kMaxPes];       // [2][T_max]
+    int64_t R_max, T_max, Y_rows;
+
+    // plan (local)
+    PlanHeader* hdr;
+    SendTile* send;
+    Group* groups;
+    RecvTile* recv;
+    Group* cgroups;
+    uint32_t* group_ctr;
+    uint32_t* cgroup_ctr;
+    uint32_t* tile_ctr;
+    int32_t max_send, max_recv;
+
+    unsigned long long* stats;  // [kStatCount]
+};
+
+}  // namespace perseus

@@ -1,0 +1,104 @@
+// perseus_internal.h — shared host/device types of libperseus.so (not part of
+// the public ABI).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "sigsim/sim.hpp"
+
+namespace perseus {
+
+// ----------------------------------------------------------- error glue ----
+struct VerifyError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+void set_last_error(const std::string& msg);
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const sigsim::ConfigError& e) {
+        set_last_error(std::string("ConfigError: ") + e.what());
+        return 1;
+    } catch (const VerifyError& e) {
+        set_last_error(std::string("VerifyError: ") + e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return 3;
+    }
+}
+
+// ------------------------------------------------------- device plan ----
+constexpr int kTileRows = 128;     // transfer tile == GEMM M-tile (PERSEUS_TILE_ROWS)
+constexpr int kMaxPes = 8;
+
+// One transfer tile this rank sends in the dispatch phase — the device
+// realisation of one reference TransferSpec tile (workload.hpp:42-49).
+struct SendTile {
+    int32_t expert;    // global expert id
+    int32_t dst;       // destination PE (== e % P)
+    int32_t row0;      // first row inside the expert's sorted segment
+    int32_t rows;      // <= kTileRows
+    int64_t heap_row;  // first destination row in dst's receive heap
+    int32_t tile_id;   // reference tile id == flag word id (-1: self segment)
+    int32_t group;     // signal group (-1: self segment, no signal)
+};
+
+// Signal group: members are a contiguous run of the tile list in the
+// reference's (dst, expert, tile) order (assign_groups, protocols.cpp:52-94).
+struct Group {
+    int32_t peer;   // destination of the group's signals
+    int32_t first;  // first member index
+    int32_t count;  // members (== target)
+    int32_t pad;
+};
+
+// One M-tile of expert-FFN work at this rank (a received transfer tile, or a
+// tile of this rank's own tokens for a local expert).
+struct RecvTile {
+    int32_t src;       // PE that owns the tokens (combine destination)
+    int32_t e_local;   // local expert index (global e = rank + P*e_local)
+    int32_t rows;
+    int32_t tile_id;   // dispatch flag id (-1: self)
+    int64_t heap_row;  // first A row in the receive heap
+    int64_t ybuf_row;  // first row in src's combine buffer (src's sorted slot)
+    int32_t cgroup;    // combine-direction signal group (-1: self)
+    int32_t pad;
+};
+
+struct PlanHeader {
+    int32_t n_send;         // send tiles (remote first, then self)
+    int32_t n_send_remote;
+    int32_t n_groups;
+    int32_t n_recv;         // recv tiles (self first, then remote)
+    int32_t n_recv_remote;
+    int32_t n_cgroups;
+    int32_t total_tiles;    // reference tile ids in use (all PEs)
+    int32_t error;
+    int64_t remote_rows_in; // rows received from peers (heap rows before the self segment)
+};
+
+// Device statistics, one slot per counter (perseus_counters order).
+enum StatSlot : int {
+    kStatDispatchFences = 0,
+    kStatDispatchSignals,
+    kStatDispatchPuts,
+    kStatDispatchBytes,
+    kStatCombineFences,
+    kStatCombineSignals,
+    kStatCombinePuts,
+    kStatCombineBytes,
+    kStatRecvTiles,
+    kStatTimeouts,
+    kStatErrors,
+    kStatCount
+};
+
+constexpr uint64_t kWaitTimeoutNs = 4000000000ull;  // 4 s: a lost signal errors out, never hangs
+
+}  // namespace perseus

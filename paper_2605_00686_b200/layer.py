@@ -1,0 +1,162 @@
+"""MoELayer — the user-facing handle of one expert-parallel rank of the B200
+Perseus MoE layer (the C ABI perseus_layer_* of include/perseus.h).
+
+It replaces the reference's hot path, ``run_dispatch`` (protocols.cpp:346-362,
+a simulator of the dispatch puts/signals with a timing stand-in for the expert
+FFN), with the real layer forward on the GPU: gate/route -> permutation ->
+dispatch puts + signals over NVLink -> SwiGLU expert FFN on tcgen05 -> combine
+puts + signals -> weighted reduce.  torch is used only for device memory,
+streams and the multi-process bootstrap.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .sigsim import ModelConfig, ProtocolConfig, combined_protocol
+
+ROUTING = {"balanced": _lib.ROUTE_BALANCED, "zipf": _lib.ROUTE_ZIPF, "gate": _lib.ROUTE_GATE}
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+class MoELayer:
+    def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
+                 device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
+                 protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True):
+        protocol = protocol or combined_protocol(0)
+        self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
+        self.routing_mode, self.skew, self.seed, self.protocol = routing, skew, seed, protocol
+        cfg = _lib.LayerConfig(model.hidden_dim, model.intermediate_dim, model.experts, model.top_k,
+                               tokens_per_pe, ROUTING[routing], float(skew), seed,
+                               protocol.device_signaling(), protocol.group_size,
+                               _lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
+        self._cfg = cfg
+        h = C.c_void_p()
+        check(lib.perseus_layer_create(C.byref(cfg), rank, world, device, C.byref(h)))
+        self._h = h
+
+    # ------------------------------------------------------------ bootstrap --
+    def ipc_blob(self) -> bytes:
+        n = C.c_size_t(0)
+        check(lib.perseus_layer_ipc_export(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib.perseus_layer_ipc_export(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def connect_ipc(self, blobs: Sequence[bytes]) -> None:
+        each = len(blobs[0])
+        data = b"".join(blobs)
+        check(lib.perseus_layer_ipc_import(self._h, data, each))
+
+    def connect_dist(self, group=None) -> None:
+        """Exchange symmetric-heap IPC handles over torch.distributed (one
+        process per GPU)."""
+        import torch.distributed as dist
+        blobs: List[bytes] = [b""] * self.world
+        dist.all_gather_object(blobs, self.ipc_blob(), group=group)
+        self.connect_ipc(blobs)
+
+    @staticmethod
+    def connect_local(layers: Sequence["MoELayer"]) -> None:
+        """P ranks emulated in one process (one device): raw peer pointers."""
+        arr = (C.c_void_p * len(layers))(*[l._h.value for l in layers])
+        check(lib.perseus_layer_connect_local(arr, len(layers)))
+
+    # -------------------------------------------------------------- weights --
+    def set_weights(self, wg, w1, w2, stream=None) -> None:
+        check(lib.perseus_layer_set_weights(self._h, _ptr(wg), _ptr(w1), _ptr(w2), _stream(stream)))
+
+    def init_synthetic(self, seed: int, stream=None) -> None:
+        check(lib.perseus_layer_init_synthetic(self._h, seed, _stream(stream)))
+
+    def fill_synthetic_x(self, x, seed: Optional[int] = None, stream=None) -> None:
+        check(lib.perseus_fill_synthetic_x(self._h, _ptr(x), self.seed if seed is None else seed,
+                                           _stream(stream)))
+
+    # -------------------------------------------------------------- forward --
+    def forward(self, x, out, stream=None) -> None:
+        check(lib.perseus_layer_forward(self._h, _ptr(x), _ptr(out), _stream(stream)))
+
+    def forward_phase(self, phase: int, x, out, stream=None) -> None:
+        check(lib.perseus_layer_forward_phase(self._h, phase, _ptr(x), _ptr(out), _stream(stream)))
+
+    def forward_host(self, x_host: np.ndarray, out_host: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+        """End-to-end entry: HOST bf16 bits [S, H] (uint16) in, HOST bf16 bits out."""
+        x_host = np.ascontiguousarray(x_host, dtype=np.uint16)
+        if out_host is None:
+            out_host = np.empty_like(x_host)
+        check(lib.perseus_layer_forward_host(self._h, x_host.ctypes.data, out_host.ctypes.data,
+                                             None if stream is None else _stream(stream)))
+        return out_host
+
+    # ------------------------------------------------------------- evidence --
+    def counters(self) -> Dict[str, int]:
+        c = _lib.Counters()
+        check(lib.perseus_layer_counters(self._h, C.byref(c)))
+        return c.as_dict()
+
+    def routing(self):
+        Sk = self.S * self.model.top_k
+        ids = np.zeros(Sk, dtype=np.int32)
+        w = np.zeros(Sk, dtype=np.float32)
+        cnt = np.zeros(self.model.experts, dtype=np.int32)
+        pos = np.zeros(Sk, dtype=np.int32)
+        P = C.POINTER
+        check(lib.perseus_layer_read_routing(self._h, ids.ctypes.data_as(P(C.c_int32)),
+                                             w.ctypes.data_as(P(C.c_float)),
+                                             cnt.ctypes.data_as(P(C.c_int32)),
+                                             pos.ctypes.data_as(P(C.c_int32))))
+        k = self.model.top_k
+        return ids.reshape(-1, k), w.reshape(-1, k), cnt, pos.reshape(-1, k)
+
+    def layout(self):
+        """(sent remote transfer tiles as an [n, 6] int64 array in TransferSpec
+        field order, flag ids observed set at this rank this forward)."""
+        n, nf = C.c_size_t(0), C.c_size_t(0)
+        check(lib.perseus_layer_read_layout(self._h, None, 0, C.byref(n), None, 0, C.byref(nf)))
+        arr = (_lib.Transfer * max(n.value, 1))()
+        flags = (C.c_int64 * max(nf.value, 1))()
+        check(lib.perseus_layer_read_layout(self._h, arr, n.value, C.byref(n), flags, nf.value,
+                                            C.byref(nf)))
+        sent = np.array([(arr[i].src_pe, arr[i].dst_pe, arr[i].expert, arr[i].bytes, arr[i].tile_id,
+                          arr[i].heap_offset) for i in range(n.value)], dtype=np.int64).reshape(-1, 6)
+        return sent, np.array(flags[:nf.value], dtype=np.int64)
+
+    def count_table(self) -> np.ndarray:
+        t = np.zeros((self.world, self.model.experts), dtype=np.int32)
+        check(lib.perseus_layer_read_count_table(self._h, t.ctypes.data_as(C.POINTER(C.c_int32))))
+        return t
+
+    def timing(self) -> List[float]:
+        ms = (C.c_float * 4)()
+        check(lib.perseus_layer_read_timing(self._h, ms, 4))
+        return list(ms)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            check(lib.perseus_layer_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
