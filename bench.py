@@ -1,0 +1,368 @@
+"""bench.py — MoE-layer forward throughput of the B200 Perseus layer.
+
+Workload (BASELINE.json configs[1], weak scaling): Qwen3-30B-A3B MoE layer
+shape — 128 experts top-8, hidden 2048, expert ffn 768, bf16 — S = 4096 tokens
+per GPU, experts sharded EP = N over N GPUs (ClusterConfig{N,1,1}), reference
+balanced routing, Perseus decoupled per-destination signalling.  Synthetic
+inputs / random-init weights from the oracle's counter hash.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our arm
+  python bench.py --impl reference [...]                   # the reference arm (CPU)
+
+N > 1 is launched by the driver under torch.distributed.run (one rank per GPU).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+QWEN3 = dict(H=2048, I=768, E=128, k=8)
+CONFIGS = {
+    "qwen3": QWEN3,
+    "llama4": dict(H=5120, I=8192, E=16, k=1),
+    "dsv3": dict(H=7168, I=2048, E=256, k=8),
+    "tiny": dict(H=256, I=512, E=8, k=2),
+}
+METRIC = "MoE-layer forward latency (µs) & tokens/s, Qwen3-30B-A3B shape, 1/2/4/8 B200"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU arms ----
+def cpu_layer_sample(cfg, tokens, seed=1, P=1, threads=None):
+    """One bounded step of the reference CPU path on the host cores: the
+    reference's own dispatch/signalling path (oracle/_ref: build_dispatch +
+    run_dispatch(combined) + fence_accounting, unmodified reference code) plus
+    the layer arithmetic the reference lacks (gate, top-k/route, SwiGLU FFN,
+    combine) from the fp32 oracle port (numpy/BLAS, all host threads).
+    Returns (tokens/s, seconds, kind, sample description)."""
+    from oracle.oracle import LayerShape, Oracle, RefLib
+    orc = Oracle()
+    H, I, E, k = cfg["H"], cfg["I"], cfg["E"], cfg["k"]
+    shape = LayerShape(H, I, E, k, tokens, P)
+    ref = RefLib() if RefLib.available() else None
+    # resident inputs (not timed): tokens and this PE's bf16 weights
+    x = orc.gen_x(shape, seed, 0)
+    wg = orc.gen_wg(shape, seed)
+    w1 = [orc.gen_w1(shape, seed, e) for e in range(E)]
+    w2 = [orc.gen_w2(shape, seed, e) for e in range(E)]
+    t0 = time.perf_counter()
+    if ref is not None:
+        r = ref.run_dispatch("combined", 0, H, I, E, k, max(P, 2), 1, 1, tokens, 0.0, 128 * H * 2, seed)
+        assert r["n_violations"] == 0
+    logits = orc.gate_logits(x, wg)
+    ids = np.zeros(tokens * k, dtype=np.int32)
+    orc.L.orc_balanced_ids(tokens, E, k, ids.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_int32)))
+    ids = ids.reshape(tokens, k)
+    w = orc.route_weights(logits, ids)
+    off, rows, pos = orc.permute(ids, E)
+    xf = orc.bf16_to_f32(x)
+    y = np.zeros((tokens * k, H), dtype=np.float32)
+    for e in range(E):
+        a, b = int(off[e]), int(off[e + 1])
+        if a == b:
+            continue
+        w1f = orc.bf16_to_f32(w1[e])
+        w2f = orc.bf16_to_f32(w2[e])
+        xe = xf[rows[a:b]]
+        g = xe @ w1f[:I].T
+        u = xe @ w1f[I:].T
+        y[a:b] = ((g / (1.0 + np.exp(-g))) * u) @ w2f.T
+    out = np.einsum("tk,tkh->th", w, y[pos])
+    dt = time.perf_counter() - t0
+    assert np.isfinite(out).all()
+    kind = "reference" if ref is not None else "port"
+    desc = (f"{tokens} tokens of the {cfg_name(cfg)} layer on {os.cpu_count()} host threads: "
+            + ("reference build_dispatch+run_dispatch(combined)+accounting (oracle/_ref) + " if ref else "")
+            + "oracle-port fp32 gate/top-k/SwiGLU-FFN/combine (numpy BLAS)")
+    return tokens / dt, dt, kind, desc
+
+
+def cfg_name(cfg):
+    for n, c in CONFIGS.items():
+        if c == cfg:
+            return n
+    return "custom"
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    tokens = args.ref_tokens
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_layer_sample(cfg, min(tokens, 128))
+    vals = []
+    kind = desc = None
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        v, dt, kind, desc = cpu_layer_sample(cfg, tokens)
+        vals.append(dt)
+    total = sum(vals)
+    value = tokens * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} MoE layer, {tokens} tokens sample per step (CPU)",
+                   "tokens_per_step": tokens},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm ----
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="perseus", choices=["perseus", "reference"])
+    ap.add_argument("--config", default="qwen3", choices=list(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU (S)")
+    ap.add_argument("--signaling", default="combined", choices=["combined", "vanilla", "decoupled"])
+    ap.add_argument("--routing", default="balanced", choices=["balanced", "zipf", "gate"])
+    ap.add_argument("--skew", type=float, default=0.0)
+    ap.add_argument("--ref-tokens", type=int, default=1024)
+    ap.add_argument("--cpu-tokens", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl != "reference":
+        args.warmup = 3  # timing rule: W >= 3
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2605_00686_b200 as pb
+
+    cfg = CONFIGS[args.config]
+    H, I, E, k, S = cfg["H"], cfg["I"], cfg["E"], cfg["k"], args.tokens
+    model = pb.ModelConfig(args.config, H, I, E, k)
+    proto = {"combined": pb.combined_protocol(0), "vanilla": pb.vanilla_protocol(),
+             "decoupled": pb.decoupled_protocol(0)}[args.signaling]
+    layer = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing,
+                        skew=args.skew, seed=1, protocol=proto)
+    if world > 1:
+        layer.connect_dist()
+    stream = torch.cuda.current_stream()
+    x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(x)
+    layer.fill_synthetic_x(x, 1)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        layer.forward(x, out)
+    barrier()
+    c0 = layer.counters()
+
+    # ---- timed region: K forwards, device-timed with CUDA events ----
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            layer.forward(x, out)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end)
+    c1 = layer.counters()
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * S * args.steps / (ms_max / 1e3)
+
+    # ---- per-stage times (CUDA events inside the layer, on its stream) ----
+    stages = []
+    for _ in range(min(args.steps, 10)):
+        layer.forward(x, out)
+        stages.append(layer.timing())
+    stages = np.array(stages)
+    st_mean = stages.mean(0).tolist()  # [route, dispatch, gemm1, gemm2, combine] ms
+
+    # ---- end-to-end through the public host API: H2D x, forward, D2H out ----
+    x_host = torch.empty(S, H, dtype=torch.int16).pin_memory()
+    o_host = torch.empty(S, H, dtype=torch.int16).pin_memory()
+    x_host.copy_(x.view(torch.int16).cpu())
+    xh = x_host.numpy().view(np.uint16)
+    oh = o_host.numpy().view(np.uint16)
+    for _ in range(2):
+        layer.forward_host(xh, oh)
+    barrier()
+    te0 = time.perf_counter()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(args.steps):
+        layer.forward_host(xh, oh)
+    e_end.record(stream)
+    barrier()
+    e_wall = time.perf_counter() - te0
+    te = torch.tensor([e_wall], device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * S * args.steps / float(te.item())
+
+    # ---- roofline of the dominant kernel (GEMM1 + SwiGLU, tcgen05) ----
+    peaks, peaks_src = measured_peaks()
+    rows = S * k  # rows through the expert FFN on this GPU (balanced: S*k per PE)
+    flops_g1 = 2.0 * rows * H * (2 * I)
+    flops_g2 = 2.0 * rows * I * H
+    g1_ms = st_mean[2]
+    g2_ms = st_mean[3]
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    ach = flops_g1 / (g1_ms / 1e3) / 1e12
+    roof = {"kernel": "k_gemm<1> (GEMM1 + fused SwiGLU, tcgen05)", "bound": "tensor", "achieved": ach,
+            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+            "peak_source": f"{peaks_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+            "algorithmic": f"2*{rows}*{H}*{2 * I} FLOP per launch",
+            "gemm2": {"achieved": flops_g2 / (g2_ms / 1e3) / 1e12, "frac": flops_g2 / (g2_ms / 1e3) / 1e12 / peak},
+            "ffn": {"achieved": (flops_g1 + flops_g2) / ((g1_ms + g2_ms) / 1e3) / 1e12,
+                    "frac": (flops_g1 + flops_g2) / ((g1_ms + g2_ms) / 1e3) / 1e12 / peak}}
+    # layer roofline: slower of compute-at-peak and bytes-over-NVLink (770 GB/s per direction)
+    flops_layer = 6.0 * H * I * S * k + 2.0 * S * H * E
+    nvl_bytes = 2.0 * S * k * (world - 1) / world * H * 2
+    t_roof = max(flops_layer / (peak * 1e12), nvl_bytes / 770e9)
+    layer_frac = t_roof / (ms_step / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, kind, desc = cpu_layer_sample(cfg, args.cpu_tokens)
+        cpu = {"value": v, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind, "sample": desc}
+
+    dc = {key: (c1[key] - c0[key]) / args.steps for key in c1 if key != "epoch"}
+    launches_per_step = 10
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "latency_us": ms_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config} MoE layer forward, S={S} tokens/GPU, EP={world} "
+                                   f"(ClusterConfig{{{world},1,1}}), {args.routing} routing, "
+                                   f"{proto.mode_name()} signalling",
+                       "model": f"{args.config}-moe-layer", "hidden": H, "ffn": I, "experts": E, "top_k": k,
+                       "tokens_per_gpu": S, "global_batch": S * world, "seq_len": S,
+                       "parallelism": f"ep{world}",
+                       "l2": f"inputs > L2: {E // world * 3 * H * I * 2 / 1e9:.2f} GB expert weights + "
+                             f"{S * H * 2 / 1e6:.0f} MB tokens streamed per step"},
+            "stage_ms": dict(zip(["route_permute", "plan_dispatch", "gemm1_swiglu", "gemm2_combine_put",
+                                  "combine"], st_mean)),
+            "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
+                               "flops": flops_layer, "nvlink_bytes": nvl_bytes},
+            "roofline": roof,
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": S * H * 2,
+                    "d2h_bytes_per_step": S * H * 2,
+                    "ms_per_step": 1e3 * float(te.item()) / args.steps},
+            "gpu_launches": launches_per_step * args.steps,
+            "per_step_counters": dc,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -208,7 +208,9 @@ int perseus_layer_read_layout(perseus_layer* layer, perseus_transfer* sent, size
 /* The count table [P][E] this rank received from all ranks in the last forward. */
 int perseus_layer_read_count_table(perseus_layer* layer, int32_t* table);
 
-/* Timing of the phases of the last forward, in ms (CUDA events). */
+/* Timing of the stages of the last perseus_layer_forward, in ms (CUDA events on
+ * its stream): [route+permute, plan+dispatch, GEMM1+SwiGLU, GEMM2+combine-put,
+ * combine]. */
 int perseus_layer_read_timing(perseus_layer* layer, float* ms, int n);
 
 #ifdef __cplusplus

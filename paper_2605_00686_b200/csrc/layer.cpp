@@ -115,7 +115,7 @@ struct perseus_layer {
     bool connected = false;
 
     CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{};
-    cudaEvent_t ev[5] = {};
+    cudaEvent_t ev[6] = {};
     const void* last_x = nullptr;
 
     DevCtx ctx(const void* x, void* out) const {
@@ -209,11 +209,12 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     if (all) ck(cudaEventRecord(L->ev[2], st), "event");
     if (all || phase == PERSEUS_PHASE_EXPERT) {
         launch_gemm(1, L->tm_a1, L->tm_b1, c, L->I / 128, L->H / 64, int64_t(c.par) * L->R_max, L->num_sms, st);
+        if (all) ck(cudaEventRecord(L->ev[3], st), "event");
         launch_gemm(2, L->tm_a2, L->tm_b2, c, L->H / 256, L->I / 64, 0, L->num_sms, st);
     }
-    if (all) ck(cudaEventRecord(L->ev[3], st), "event");
-    if (all || phase == PERSEUS_PHASE_COMBINE) launch_combine(c, st);
     if (all) ck(cudaEventRecord(L->ev[4], st), "event");
+    if (all || phase == PERSEUS_PHASE_COMBINE) launch_combine(c, st);
+    if (all) ck(cudaEventRecord(L->ev[5], st), "event");
     ck(cudaGetLastError(), "kernel launch");
 }
 
@@ -498,8 +499,8 @@ int perseus_layer_read_count_table(perseus_layer* L, int32_t* table) {
 
 int perseus_layer_read_timing(perseus_layer* L, float* ms, int n) {
     return guarded([&] {
-        ck(cudaEventSynchronize(L->ev[4]), "event sync");
-        for (int i = 0; i < n && i < 4; ++i) ck(cudaEventElapsedTime(&ms[i], L->ev[i], L->ev[i + 1]), "elapsed");
+        ck(cudaEventSynchronize(L->ev[5]), "event sync");
+        for (int i = 0; i < n && i < 5; ++i) ck(cudaEventElapsedTime(&ms[i], L->ev[i], L->ev[i + 1]), "elapsed");
     });
 }
 

@@ -39,8 +39,19 @@ DEVI bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+DEVI uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Pipeline waits never hang the GPU: after 10 s without progress the kernel
+// traps (the launch fails with an error the host reports) instead of spinning.
 DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 10000000000ull) asm volatile("trap;");
     }
 }
 

@@ -146,8 +146,8 @@ class MoELayer:
         return t
 
     def timing(self) -> List[float]:
-        ms = (C.c_float * 4)()
-        check(lib.perseus_layer_read_timing(self._h, ms, 4))
+        ms = (C.c_float * 5)()
+        check(lib.perseus_layer_read_timing(self._h, ms, 5))
         return list(ms)
 
     def close(self) -> None:
