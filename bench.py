@@ -64,7 +64,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -196,7 +196,7 @@ def run_reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="perseus", choices=["perseus", "reference"])
     ap.add_argument("--config", default="qwen3", choices=list(CONFIGS))
@@ -249,6 +249,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(local).__enter__()  # samples across warm-up, timed region and e2e loop
+    t_wait = time.time()
+    while not clk.lines and time.time() - t_wait < 3.0:
+        time.sleep(0.02)
     for _ in range(args.warmup):
         layer.forward(x, out)
     barrier()
@@ -256,13 +260,14 @@ def main():
 
     # ---- timed region: K forwards, device-timed with CUDA events ----
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        start.record(stream)
-        for _ in range(args.steps):
-            layer.forward(x, out)
-        end.record(stream)
-        barrier()
+    n_clk0 = len(clk.lines)
+    barrier()
+    start.record(stream)
+    for _ in range(args.steps):
+        layer.forward(x, out)
+    end.record(stream)
+    barrier()
+    n_clk1 = len(clk.lines)
     ms = start.elapsed_time(end)
     c1 = layer.counters()
     t = torch.tensor([ms], device="cuda")
@@ -301,6 +306,7 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * S * args.steps / float(te.item())
+    clk.__exit__(None, None, None)
 
     # ---- roofline of the dominant kernel (GEMM1 + SwiGLU, tcgen05) ----
     peaks, peaks_src = measured_peaks()
@@ -355,7 +361,7 @@ def main():
                     "ms_per_step": 1e3 * float(te.item()) / args.steps},
             "gpu_launches": launches_per_step * args.steps,
             "per_step_counters": dc,
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), timed_region_samples=n_clk1 - n_clk0),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -8,10 +8,13 @@
 #include "layer_dev.h"
 #include "perseus.h"
 #include "ptx.cuh"
+#include "signal.cuh"
 
 namespace perseus {
 
 using namespace ptx;
+
+size_t perm_smem_bytes(const DevCtx& c);
 
 // ------------------------------------------------------------ synthetic ----
 // Same counter hash as oracle/oracle.c:orc_fill_bf16 (bit-identical bf16).
@@ -152,61 +155,69 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
 }
 
 // ----------------------------------------------------------- permutation ----
-__global__ void __launch_bounds__(256) k_count(DevCtx c) {
+// Stable counting sort of the (token, j) pairs by expert (orc_permute): tokens
+// ascending inside each expert segment.  Two passes over 256-token blocks:
+//   k_hist : per-block expert histogram           hist[b][e]
+//   k_perm : segment offsets (scan), then stable in-block ranks from a
+//            per-expert token bitmask (popcount of the lower lanes).
+constexpr int kPermT = 256;
+
+__global__ void __launch_bounds__(kPermT) k_hist(DevCtx c) {
     extern __shared__ int32_t hist[];
     for (int e = threadIdx.x; e < c.E; e += blockDim.x) hist[e] = 0;
     __syncthreads();
-    const int64_t n = int64_t(c.S) * c.k;
-    const int64_t i0 = int64_t(blockIdx.x) * 4096;
-    for (int64_t i = i0 + threadIdx.x; i < n && i < i0 + 4096; i += blockDim.x) atomicAdd(&hist[c.ids[i]], 1);
+    const int t = blockIdx.x * kPermT + threadIdx.x;
+    if (t < c.S)
+        for (int j = 0; j < c.k; ++j) atomicAdd(&hist[c.ids[size_t(t) * c.k + j]], 1);
     __syncthreads();
-    for (int e = threadIdx.x; e < c.E; e += blockDim.x)
-        if (hist[e]) atomicAdd(&c.counts[e], hist[e]);
+    for (int e = threadIdx.x; e < c.E; e += blockDim.x) c.hist[size_t(blockIdx.x) * c.E + e] = hist[e];
 }
 
-// Stable counting-sort scatter: one CTA per expert walks the (token, j) pairs
-// in order and ranks its matches with warp ballots (orc_permute).
-__global__ void __launch_bounds__(1024) k_scatter(DevCtx c) {
-    __shared__ int32_t wsum[32];
-    __shared__ int32_t s_base, s_off;
-    const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        int32_t o = 0;
-        for (int q = 0; q < e; ++q) o += c.counts[q];
-        s_off = o;
-        s_base = 0;
-        c.offsets[e] = o;
-        if (e == c.E - 1) c.offsets[c.E] = o + c.counts[e];
+__device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33*/);
+
+__global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
+    extern __shared__ int32_t sm[];
+    const int E = c.E, b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
+    uint32_t* bits = reinterpret_cast<uint32_t*>(sm);  // [E][kPermT / 32]
+    int32_t* base = sm + E * (kPermT / 32);             // [E]
+    int32_t* tot = base + E;                            // [E]
+    int32_t* scratch = tot + E;                         // [33]
+    for (int i = tid; i < E * (kPermT / 32); i += kPermT) bits[i] = 0;
+    for (int e = tid; e < E; e += kPermT) {
+        int32_t before = 0, after = 0;
+        for (int q = 0; q < nb; ++q) {
+            const int32_t v = c.hist[size_t(q) * E + e];
+            if (q < b) before += v; else after += v;
+        }
+        base[e] = before;
+        tot[e] = before + after;
+        if (b == 0) c.counts[e] = before + after;
     }
     __syncthreads();
-    const int32_t off = s_off;
-    const int64_t n = int64_t(c.S) * c.k;
-    for (int64_t i0 = 0; i0 < n; i0 += 1024) {
-        const int64_t i = i0 + tid;
-        const bool m = i < n && c.ids[i] == e;
-        const unsigned bal = __ballot_sync(0xffffffffu, m);
-        if (lane == 0) wsum[warp] = __popc(bal);
-        __syncthreads();
-        if (warp == 0) {
-            const int v = wsum[lane];
-            int incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            wsum[lane] = incl - v;
+    const int32_t total = block_exclusive_scan(tot, E, scratch);
+    for (int e = tid; e < E; e += kPermT) {
+        base[e] += tot[e];
+        if (b == 0) c.offsets[e] = tot[e];
+    }
+    if (b == 0 && tid == 0) c.offsets[E] = total;
+    const int t = b * kPermT + tid;
+    int32_t my[16];
+    if (t < c.S)
+        for (int j = 0; j < c.k; ++j) {
+            my[j] = c.ids[size_t(t) * c.k + j];
+            atomicOr(&bits[my[j] * (kPermT / 32) + (tid >> 5)], 1u << (tid & 31));
         }
-        __syncthreads();
-        const int32_t base = s_base;
-        if (m) {
-            const int32_t r = off + base + wsum[warp] + __popc(bal & ((1u << lane) - 1u));
-            c.rows[r] = int32_t(i / c.k);
-            c.pos[i] = r;
-        }
-        __syncthreads();
-        if (tid == 1023) s_base = base + wsum[31] + __popc(bal);
-        __syncthreads();
+    __syncthreads();
+    if (t >= c.S) return;
+    const int w = tid >> 5;
+    const uint32_t below = (1u << (tid & 31)) - 1u;
+    for (int j = 0; j < c.k; ++j) {
+        const uint32_t* row = bits + my[j] * (kPermT / 32);
+        int32_t rank = __popc(row[w] & below);
+        for (int q = 0; q < w; ++q) rank += __popc(row[q]);
+        const int32_t p = base[my[j]] + rank;
+        c.rows[p] = t;
+        c.pos[size_t(t) * c.k + j] = p;
     }
 }
 
@@ -226,10 +237,11 @@ __global__ void __launch_bounds__(256) k_publish_counts(DevCtx c) {
 }
 
 // ------------------------------------------------------------------ plan ----
-// Block-wide exclusive scan of n ints in shared memory (1024 threads).
-__device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*32*/) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (n + 1023) / 1024;
+// Block-wide exclusive scan of n ints in shared memory (any blockDim that is a
+// multiple of 32); returns the total.  Must be called by every thread.
+__device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33*/) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
     const int b = tid * per;
     int32_t local = 0;
     for (int i = 0; i < per; ++i)
@@ -243,7 +255,7 @@ __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*32
     if (lane == 31) scratch[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        const int32_t v = scratch[lane];
+        const int32_t v = lane < nwarps ? scratch[lane] : 0;
         int32_t wi = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -500,22 +512,6 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
     }
 }
 
-// ---------------------------------------------------------- signalling ----
-// Phase 2 of Alg. 1 for one group, executed by the thread that completed the
-// group's counter: ONE sys-scope fence, then every member's flag word in
-// member order (protocols.cpp:275-292).  With suppress (fault injection) the
-// fence is dropped (transport.cpp:104-106).
-template <class FlagOf>
-__device__ void signal_group(const DevCtx& c, const Group& g, FlagOf flag_of, bool suppress,
-                             int stat_fence, int stat_signal) {
-    if (!suppress) {
-        fence_acq_rel_sys();
-        atomicAdd(&c.stats[stat_fence], 1ull);
-    }
-    for (int m = 0; m < g.count; ++m) st_relaxed_sys(flag_of(g.first + m), c.epoch);
-    atomicAdd(&c.stats[stat_signal], (unsigned long long)g.count);
-}
-
 // -------------------------------------------------------------- dispatch ----
 // One CTA per send tile: gather the tile's token rows (sorted order) and store
 // them into the destination's receive heap — a one-sided NVLink store for a
@@ -547,24 +543,18 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
     }
     if (st.dst == c.rank) return;  // self segment: ordered by the stream, no signal
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
-    atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
-    const bool suppress = c.signaling == PERSEUS_SIGNAL_NONE;
+    if (warp != 0) return;
+    if (lane == 0) {
+        atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
+        atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
+    }
     const Group g = c.groups[st.group];
     auto flag_of = [&](int m) {
         const SendTile& t = c.send[m];
         return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
     };
-    if (g.count == 1) {
-        signal_group(c, g, flag_of, suppress, kStatDispatchFences, kStatDispatchSignals);
-    } else {
-        // Phase 1: publish this tile into the group counter (gpu-scope
-        // release covers the CTA's stores via the barrier above).
-        const uint32_t old = atom_add_acq_rel_gpu(c.group_ctr + st.group, 1u);
-        if (old + 1 == uint32_t(g.count))
-            signal_group(c, g, flag_of, suppress, kStatDispatchFences, kStatDispatchSignals);
-    }
+    publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+                        kStatDispatchFences, kStatDispatchSignals);
 }
 
 // --------------------------------------------------------------- combine ----
@@ -610,15 +600,23 @@ __global__ void __launch_bounds__(256) k_combine(DevCtx c) {
 }
 
 // ------------------------------------------------------------- launchers ----
-void launch_route(const DevCtx& c, cudaStream_t st) {
+// bit-exact CUDA-core gate (learned-gate routing)
+void launch_gate_exact(const DevCtx& c, cudaStream_t st) {
     dim3 g((c.S + kGateT - 1) / kGateT, (c.E + kGateE - 1) / kGateE);
     k_gate<<<g, 256, 0, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
+}
+
+// route + permutation + count publish (after the gate logits exist)
+void launch_route(const DevCtx& c, cudaStream_t st) {
     k_route<<<(c.S + 7) / 8, 256, 0, st>>>(c);
-    cudaMemsetAsync(c.counts, 0, sizeof(int32_t) * c.E, st);
-    const int64_t n = int64_t(c.S) * c.k;
-    k_count<<<int((n + 4095) / 4096), 256, sizeof(int32_t) * c.E, st>>>(c);
-    k_scatter<<<c.E, 1024, 0, st>>>(c);
+    const int nb = (c.S + kPermT - 1) / kPermT;
+    k_hist<<<nb, kPermT, sizeof(int32_t) * c.E, st>>>(c);
+    k_perm<<<nb, kPermT, perm_smem_bytes(c), st>>>(c);
     k_publish_counts<<<1, 256, 0, st>>>(c);
+}
+
+size_t perm_smem_bytes(const DevCtx& c) {
+    return sizeof(int32_t) * (size_t(c.E) * (kPermT / 32) + 2 * size_t(c.E) + 40);
 }
 
 size_t plan_smem_bytes(const DevCtx& c) {
@@ -636,8 +634,10 @@ void launch_combine(const DevCtx& c, cudaStream_t st) {
 }
 
 cudaError_t configure_kernels(const DevCtx& c) {
-    return cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(plan_smem_bytes(c)));
+    cudaError_t e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(plan_smem_bytes(c)));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(perm_smem_bytes(c)));
 }
 
 }  // namespace perseus

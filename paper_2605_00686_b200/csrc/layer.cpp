@@ -21,14 +21,16 @@ namespace perseus {
 
 // kernels.cu / gemm.cu
 void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, float scale, cudaStream_t st);
+void launch_gate_exact(const DevCtx& c, cudaStream_t st);
+void launch_gate_tc(const CUtensorMap& tx, const CUtensorMap& twg, const DevCtx& c, int grid, cudaStream_t st);
 void launch_route(const DevCtx& c, cudaStream_t st);
 void launch_dispatch(const DevCtx& c, cudaStream_t st);
 void launch_combine(const DevCtx& c, cudaStream_t st);
 cudaError_t configure_kernels(const DevCtx& c);
 size_t gemm_smem_bytes();
 cudaError_t configure_gemm();
-void launch_gemm(int mode, const CUtensorMap& ta, const CUtensorMap& tb, const DevCtx& c, int n_nb,
-                 int num_kb, int64_t a_row_base, int grid, cudaStream_t st);
+void launch_gemm(int mode, const CUtensorMap& ta, const CUtensorMap& tb,
+                 const DevCtx& c, int n_nb, int num_kb, int64_t a_row_base, int grid, cudaStream_t st);
 
 namespace {
 thread_local std::string g_err;
@@ -60,12 +62,13 @@ EncodeTiled encoder() {
     return fn;
 }
 
-// bf16 row-major [rows][cols] viewed as a 2D tensor, box 64 (K) x 128 rows, SW128
-CUtensorMap make_tmap(const void* base, uint64_t rows, uint64_t cols) {
+// bf16 row-major [rows][cols] viewed as a 2D tensor, box 64 (K) x box_rows, SW128
+// (box_rows = 1 for tile::gather4 maps)
+CUtensorMap make_tmap(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows = 128) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {cols, rows};
     const cuuint64_t strides[1] = {cols * 2};
-    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t box[2] = {64, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -98,7 +101,7 @@ struct perseus_layer {
     bf16 *wg = nullptr, *w1 = nullptr, *w2 = nullptr, *hbuf = nullptr;
     float *logits = nullptr, *weights = nullptr;
     int32_t *ids = nullptr, *counts = nullptr, *offsets = nullptr, *rows = nullptr, *pos = nullptr,
-            *zipf_ids = nullptr;
+            *zipf_ids = nullptr, *hist = nullptr;
     PlanHeader* hdr = nullptr;
     SendTile* send = nullptr;
     Group *groups = nullptr, *cgroups = nullptr;
@@ -114,7 +117,8 @@ struct perseus_layer {
     bool ipc_mapped[kMaxPes] = {};
     bool connected = false;
 
-    CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{};
+    CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{}, tm_wg{}, tm_x{}, tm_xg{};
+    const void* tm_x_ptr = nullptr;
     cudaEvent_t ev[6] = {};
     const void* last_x = nullptr;
 
@@ -130,6 +134,7 @@ struct perseus_layer {
         c.out = static_cast<bf16*>(out);
         c.wg = wg; c.logits = logits; c.ids = ids; c.weights = weights; c.counts = counts;
         c.offsets = offsets; c.rows = rows; c.pos = pos; c.zipf_ids = zipf_ids; c.hbuf = hbuf;
+        c.hist = hist;
         for (int p = 0; p < world; ++p) {
             uint8_t* b = peer[p];
             c.count_table[p] = reinterpret_cast<int32_t*>(b + off_ctab);
@@ -158,7 +163,7 @@ void validate(const perseus_layer_config& c, int rank, int world) {
     if (c.experts % world) throw sigsim::ConfigError("experts not divisible by PEs");
     if (c.hidden_dim % 256) throw sigsim::ConfigError("hidden_dim must be a multiple of 256");
     if (c.intermediate_dim % 128) throw sigsim::ConfigError("intermediate_dim must be a multiple of 128");
-    if (c.experts > 1024) throw sigsim::ConfigError("experts must be <= 1024");
+    if (c.experts > 256) throw sigsim::ConfigError("experts must be <= 256");
     if (c.top_k > 16) throw sigsim::ConfigError("top_k must be <= 16");
     if (int64_t(world) * c.experts > 4096) throw sigsim::ConfigError("P*E must be <= 4096");
     if (c.tokens_per_pe == 0) throw sigsim::ConfigError("tokens_per_pe must be > 0");
@@ -185,7 +190,7 @@ void free_layer(perseus_layer* L) {
     for (int p = 0; p < kMaxPes; ++p)
         if (L->ipc_mapped[p]) cudaIpcCloseMemHandle(L->peer[p]);
     void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
-                    L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hdr, L->send, L->groups,
+                    L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -201,9 +206,21 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     if (phase == PERSEUS_PHASE_ROUTE || phase == PERSEUS_PHASE_ALL) ++L->epoch;
     if (x) L->last_x = x;
     DevCtx c = L->ctx(x ? x : L->last_x, out);
+    if (c.x != L->tm_x_ptr) {  // TMA maps over the caller's token buffer (router tiles + row gathers)
+        L->tm_x = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H));
+        L->tm_xg = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H), 1);
+        L->tm_x_ptr = c.x;
+    }
     const bool all = phase == PERSEUS_PHASE_ALL;
     if (all) ck(cudaEventRecord(L->ev[0], st), "event");
-    if (all || phase == PERSEUS_PHASE_ROUTE) launch_route(c, st);
+    if (all || phase == PERSEUS_PHASE_ROUTE) {
+        if (L->cfg.routing == PERSEUS_ROUTE_GATE) {
+            launch_gate_exact(c, st);  // bit-exact fp32 order: learned top-k ids must match the oracle
+        } else {
+            launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, st);
+        }
+        launch_route(c, st);
+    }
     if (all) ck(cudaEventRecord(L->ev[1], st), "event");
     if (all || phase == PERSEUS_PHASE_DISPATCH) launch_dispatch(c, st);
     if (all) ck(cudaEventRecord(L->ev[2], st), "event");
@@ -267,6 +284,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->rows = dalloc<int32_t>(Sk);
             L->pos = dalloc<int32_t>(Sk);
             L->zipf_ids = dalloc<int32_t>(Sk);
+            L->hist = dalloc<int32_t>(((S + 255) / 256) * E);
             L->hdr = dalloc<PlanHeader>(1);
             L->send = dalloc<SendTile>(L->max_send);
             L->groups = dalloc<Group>(L->max_send);
@@ -298,6 +316,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->tm_b1 = make_tmap(L->w1, El * 2 * I, H);
             L->tm_a2 = make_tmap(L->hbuf, uint64_t(L->R_max), I);
             L->tm_b2 = make_tmap(L->w2, El * H, I);
+            L->tm_wg = make_tmap(L->wg, E, H);
             ck(configure_gemm(), "configure_gemm");
             ck(configure_kernels(L->ctx(nullptr, nullptr)), "configure_kernels");
             if (world == 1) {

@@ -31,6 +31,7 @@ struct DevCtx {
     int32_t* offsets;    // [E+1]: sorted segment starts of this rank's (token, j) pairs
     int32_t* rows;       // [S*k]: token of each sorted slot
     int32_t* pos;        // [S*k]: sorted slot of each (token, j)
+    int32_t* hist;       // [ceil(S/256)][E]: per-block expert histogram
     const int32_t* zipf_ids;  // [S*k]: reference Zipf draws (routing == ZIPF)
     bf16* hbuf;          // [R_max][I]
 

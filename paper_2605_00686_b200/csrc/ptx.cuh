@@ -68,6 +68,43 @@ DEVI void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int32_t c
         "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// 4-row gather (sm_100): rows r0..r3 of a 2D map whose box is {64, 1}; the
+// 4 x 128 B land contiguously at smem_dst with the map's swizzle applied.
+DEVI void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int32_t col, int32_t r0,
+                      int32_t r1, int32_t r2, int32_t r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1),
+        "r"(r2), "r"(r3)
+        : "memory");
+}
+// bulk copy shared -> global (any global address, incl. peer-mapped NVLink
+// memory), completion tracked by bulk async-groups of the issuing thread
+DEVI void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+DEVI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+DEVI void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+DEVI void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int N>
+DEVI void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+DEVI void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+// 16-byte global -> shared async copy (LDGSTS), L1 bypass
+DEVI void cp_async_16(uint32_t smem_addr, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gsrc) : "memory");
+}
+// the mbarrier phase cannot complete before this thread's prior cp.async land
+// (pending count +1 now, async arrive on completion)
+DEVI void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+DEVI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // generic-proxy writes observed via acquire, then read by the async proxy
 DEVI void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 

@@ -1,0 +1,92 @@
+"""Multi-GPU parity check: one process per GPU, launched by
+`python -m torch.distributed.run --nproc-per-node P tests/mgpu_check.py`.
+
+Every rank runs the real concurrent forward (dispatch puts and combine puts
+over NVLink into cudaIpc-mapped symmetric buffers, ranks synchronising only
+through device flag words), then checks — against the oracle and the
+reference layout restatement — its routing, the realised dispatch layout
+(tile ids, heap offsets), its flag words, its fence counts and its output.
+Rank 0 prints one JSON line with the verdict.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    import paper_2605_00686_b200 as pb
+    from oracle.oracle import LayerShape, Oracle, transfers_to_np
+    from tests.gpu_util import assert_close, bf16_bits
+
+    orc = Oracle()
+    cases = [
+        ("balanced", 0.0, pb.combined_protocol(0), 2048, 768, 128, 8, 512),
+        ("balanced", 0.0, pb.vanilla_protocol(), 2048, 768, 128, 8, 512),
+        ("zipf", 1.2, pb.combined_protocol(0), 1024, 512, 16 * world, 4, 768),
+        ("gate", 0.0, pb.decoupled_protocol(0), 512, 256, 8 * world, 2, 1024),
+    ]
+    results = []
+    ok = True
+    for routing, skew, proto, H, I, E, k, S in cases:
+        m = pb.ModelConfig("m", H, I, E, k)
+        layer = pb.MoELayer(m, S, rank=rank, world=world, device=local, routing=routing, skew=skew,
+                            seed=7, protocol=proto)
+        layer.connect_dist()
+        x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
+        out = torch.empty_like(x)
+        layer.fill_synthetic_x(x, 7)
+        for _ in range(3):  # repeated forwards flip the symmetric double buffers
+            layer.forward(x, out)
+        torch.cuda.synchronize()
+        dist.barrier()
+        r = {"routing": routing, "protocol": proto.mode_name(), "rank": rank}
+        try:
+            c = layer.counters()
+            assert c["wait_timeouts"] == 0 and c["errors"] == 0, c
+            table = layer.count_table()
+            R, nr, _, _ = orc.layout_from_counts(table.astype(np.uint64), H, E, world, 1, 128 * H * 2)
+            want = transfers_to_np(R, nr)
+            sent, flags = layer.layout()
+            assert np.array_equal(sent, want[want[:, 0] == rank]), "sent layout != reference"
+            assert np.array_equal(np.sort(flags), np.sort(want[want[:, 1] == rank, 4])), "flags"
+            own = want[want[:, 0] == rank]
+            exp = orc.fences_for_src(own, rank, 0 if proto.signaling == "coupled" else 1, proto.group_size)
+            per_fwd = c["dispatch_fences"] / 3
+            assert per_fwd == exp, (per_fwd, exp)
+            shape = LayerShape(H, I, E, k, S, world)
+            ids, w, counts, pos = layer.routing()
+            ref, ids_o, w_o = orc.layer_forward(shape, routing, 7, rank, skew)
+            assert np.array_equal(ids, ids_o), "ids"
+            got = orc.bf16_to_f32(bf16_bits(out))
+            rel = assert_close(got, ref, what=f"{routing}/{proto.mode_name()} rank {rank}")
+            r.update(ok=True, fences_per_forward=per_fwd, signals=c["dispatch_signals"] / 3,
+                     rel_err=[float(rel[0]), float(rel[1])], n_sent=int(len(sent)))
+        except AssertionError as e:
+            ok = False
+            r.update(ok=False, error=str(e)[:300])
+        all_r = [None] * world
+        dist.all_gather_object(all_r, r)
+        results.append(all_r)
+        layer.close()
+        dist.barrier()
+    if rank == 0:
+        verdict = all(rr["ok"] for res in results for rr in res)
+        print(json.dumps({"mgpu_check": "pass" if verdict else "FAIL", "world": world, "results": results}))
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
