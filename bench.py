@@ -207,6 +207,7 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=1024)
     ap.add_argument("--cpu-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="stage kernels instead of the fused persistent kernel")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3  # timing rule: W >= 3
@@ -235,7 +236,7 @@ def main():
     proto = {"combined": pb.combined_protocol(0), "vanilla": pb.vanilla_protocol(),
              "decoupled": pb.decoupled_protocol(0)}[args.signaling]
     layer = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing,
-                        skew=args.skew, seed=1, protocol=proto)
+                        skew=args.skew, seed=1, protocol=proto, fused=not args.unfused)
     if world > 1:
         layer.connect_dist()
     stream = torch.cuda.current_stream()
@@ -352,7 +353,10 @@ def main():
                        "l2": f"inputs > L2: {E // world * 3 * H * I * 2 / 1e9:.2f} GB expert weights + "
                              f"{S * H * 2 / 1e6:.0f} MB tokens streamed per step"},
             "stage_ms": dict(zip(["route_permute", "plan_dispatch", "gemm1_swiglu", "gemm2_combine_put",
-                                  "combine"], st_mean)),
+                                  "combine"] if args.unfused else
+                                 ["route_permute", "plan", "fused_dispatch_ffn_combineput", "-", "combine"],
+                                 st_mean)),
+            "fused": not args.unfused,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes},
             "roofline": roof,

@@ -125,6 +125,7 @@ typedef struct perseus_layer_config {
 } perseus_layer_config;
 
 #define PERSEUS_F_SYNTH_WEIGHTS 1 /* generate weights on device from `seed` */
+#define PERSEUS_F_UNFUSED 2       /* forward() as stream-ordered stage kernels instead of the fused persistent kernel */
 
 /* Tile granularity: 128 token rows per transfer tile / GEMM M-tile, i.e. the
  * reference's tile_bytes = 128 * H * 2 (workload.hpp:58). */

@@ -16,6 +16,7 @@ ROUTE_BALANCED, ROUTE_ZIPF, ROUTE_GATE = 0, 1, 2
 SIGNAL_COUPLED, SIGNAL_DECOUPLED, SIGNAL_NONE = 0, 1, 2
 PHASE_ROUTE, PHASE_DISPATCH, PHASE_EXPERT, PHASE_COMBINE, PHASE_ALL = 0, 1, 2, 3, 15
 F_SYNTH_WEIGHTS = 1
+F_UNFUSED = 2
 TILE_ROWS = 128
 
 

@@ -140,7 +140,18 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
         const int64_t flat = int64_t(t) * c.k + lane;
         my_id = c.routing == PERSEUS_ROUTE_BALANCED ? int(flat % c.E) : c.zipf_ids[flat];
     }
-    const float mine = lane < c.k ? l[my_id] : -INFINITY;
+    float mine = -INFINITY;
+    if (lane < c.k) {
+        if (c.routing == PERSEUS_ROUTE_GATE) {
+            mine = l[my_id];
+        } else {
+            // tensor-core router: sum the split-K partial logits in fixed order
+            mine = 0.f;
+            for (int q = 0; q < c.gate_splits; ++q) mine += c.logits[(size_t(q) * c.S + t) * c.E + my_id];
+        }
+        // per-256-token-block expert histogram (this forward's parity half)
+        atomicAdd(&c.hist[(size_t(c.par) * c.hist_blocks + t / 256) * c.E + my_id], 1);
+    }
     float m = mine;
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -183,17 +194,29 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     int32_t* tot = base + E;                            // [E]
     int32_t* scratch = tot + E;                         // [33]
     for (int i = tid; i < E * (kPermT / 32); i += kPermT) bits[i] = 0;
+    const int32_t* hist = c.hist + size_t(c.par) * c.hist_blocks * E;
+    int32_t* hist_next = c.hist + size_t(c.par ^ 1) * c.hist_blocks * E;  // zeroed for the next forward
     for (int e = tid; e < E; e += kPermT) {
         int32_t before = 0, after = 0;
         for (int q = 0; q < nb; ++q) {
-            const int32_t v = c.hist[size_t(q) * E + e];
+            const int32_t v = hist[size_t(q) * E + e];
             if (q < b) before += v; else after += v;
         }
         base[e] = before;
         tot[e] = before + after;
-        if (b == 0) c.counts[e] = before + after;
+        hist_next[size_t(b) * E + e] = 0;
+        if (b == 0) {
+            c.counts[e] = before + after;
+            // count exchange: this rank's row of every PE's [P][E] table
+            for (int p = 0; p < c.P; ++p) c.count_table[p][(size_t(c.par) * c.P + c.rank) * E + e] = before + after;
+        }
     }
     __syncthreads();
+    if (b == 0 && tid == 0) {
+        // one sys-scope fence, then the per-source ready flag at every PE
+        fence_acq_rel_sys();
+        for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
+    }
     const int32_t total = block_exclusive_scan(tot, E, scratch);
     for (int e = tid; e < E; e += kPermT) {
         base[e] += tot[e];
@@ -297,10 +320,12 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
     int32_t* off = hr + PE;       // sorted offsets per (s, e)
     int32_t* sp = off + PE;       // send position per e (key order)
     int32_t* rp = sp + E;         // recv position per (ks, j)
-    int32_t* scratch = rp + E;    // 33
+    int32_t* scratch = rp + E;    // 33 (+pad)
+    int32_t* selfo = scratch + 40;  // [El] self-segment row offsets
+    int32_t* tb2 = selfo + El;      // [P*E] scratch
     __shared__ int32_t s_err;
     __shared__ int32_t dst_first[kMaxPes + 1], dst_group[kMaxPes], src_first[kMaxPes + 1],
-        src_group[kMaxPes];
+        src_group[kMaxPes], dst_n[kMaxPes], src_n[kMaxPes];
 
     if (tid == 0) s_err = 0;
     if (tid < P) {
@@ -325,16 +350,14 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
     const int32_t total_hr = block_exclusive_scan(hr, PE, scratch);
     // rows received here from peers: the extent of destination block r
     const int32_t rows_in_r = (r + 1 < P ? hr[(r + 1) * P * El] : total_hr) - hr[r * P * El];
-    // per-row exclusive scans of off (sorted offsets inside each source)
-    if (tid < P) {
-        int32_t run = 0;
-        for (int e = 0; e < E; ++e) {
-            const int32_t v = off[tid * E + e];
-            off[tid * E + e] = run;
-            run += v;
-        }
-    }
+    // sorted offsets inside each source: one scan over [P][E], minus row starts
+    block_exclusive_scan(off, PE, scratch);
+    for (int i = tid; i < PE; i += 1024) tb2[i] = off[(i / E) * E];  // row start
+    // self-segment offsets of this rank's local experts (e = r + P*j)
+    for (int j = tid; j < El; j += 1024) selfo[j] = T[r * E + r + P * j];
     __syncthreads();
+    for (int i = tid; i < PE; i += 1024) off[i] -= tb2[i];
+    block_exclusive_scan(selfo, El, scratch);
 
     // ---- send side (this rank as source) ----
     // key order: remote destinations ascending, then the self segment
@@ -353,9 +376,11 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
             const int first = sp[kd * El];
             const int last = kd + 1 < P ? sp[(kd + 1) * El] : n_send;
             dst_first[d] = first;
+            dst_n[d] = last - first;
             dst_group[d] = (d != r && last > first) ? g++ : -1;
         }
         dst_first[kMaxPes] = g;
+        for (int q = 0; q < 4; ++q) c.sched[q] = 0;
     }
     __syncthreads();
     const int32_t n_send_remote = dst_first[r];
@@ -373,9 +398,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
         if (d != r) {
             hrow = hr[(d * P + r) * El + j] - hr[d * P * El];
         } else {
-            int32_t so = 0;
-            for (int jj = 0; jj < j; ++jj) so += T[r * E + r + P * jj];
-            hrow = rows_in_r + so;
+            hrow = rows_in_r + selfo[j];
         }
         for (int ch = 0; ch < nt; ++ch) {
             SendTile st;
@@ -387,7 +410,28 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
             st.tile_id = d != r ? tb[r * E + e] + ch : -1;
             const int p = pos0 + ch;
             st.group = d == r ? -1 : (gs > 0 ? p / gs : dst_group[d]);
-            if (p < c.max_send) c.send[p] = st; else s_err = 3;
+            st.recv_pos = -1;
+            st.pad = 0;
+            // copy order: tile idx-major over destinations [self, remote ascending],
+            // so every receiver sees its sources' tiles arrive interleaved
+            const int idx = ch + (pos0 - dst_first[d]);
+            int so = 0;
+            for (int q = 0; q < P; ++q) {
+                const int dq = q == 0 ? r : (q <= r ? q - 1 : q);
+                so += min(dst_n[dq], idx) + ((dq == d) ? 0 : 0);
+            }
+            for (int q = 0; q < P; ++q) {
+                const int dq = q == 0 ? r : (q <= r ? q - 1 : q);
+                if (dq == d) break;
+                so += dst_n[dq] > idx;
+            }
+            if (p < c.max_send) {
+                c.send[p] = st;
+                c.send_done[p] = 0;
+                c.sorder[so] = p;
+            } else {
+                s_err = 3;
+            }
         }
     }
     // groups (dispatch direction)
@@ -429,6 +473,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
             const int first = rp[ks * El];
             const int last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
             src_first[s] = first;
+            src_n[s] = last - first;
             src_group[s] = (s != r && last > first) ? g++ : -1;
         }
     }
@@ -450,9 +495,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
         if (s != r) {
             hrow = hr[(r * P + s) * El + j] - hr[r * P * El];
         } else {
-            int32_t so = 0;
-            for (int jj = 0; jj < j; ++jj) so += T[r * E + r + P * jj];
-            hrow = rows_in_r + so;
+            hrow = rows_in_r + selfo[j];
         }
         for (int ch = 0; ch < nt; ++ch) {
             RecvTile rt;
@@ -465,9 +508,24 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
             const int p = pos0 + ch;
             rt.cgroup = s == r ? -1 : (gs > 0 ? (p - n_recv_self) / gs : src_group[s]);
             rt.pad = 0;
-            if (p < c.max_recv) {
+            // processing order: self tiles first, then remote tiles idx-major
+            // over sources (the order the interleaved copies arrive in)
+            int ro = p;
+            if (s != r) {
+                const int idx = p - src_first[s];
+                ro = n_recv_self;
+                for (int q = 0; q < P; ++q)
+                    if (q != r) ro += min(src_n[q], idx) + ((q < s && src_n[q] > idx) ? 1 : 0);
+            } else {
+                // link the matching self send tile (self is last in send key order)
+                const int sp_self = sp[(P - 1) * El + j] + ch;
+                if (sp_self < c.max_send) c.send[sp_self].recv_pos = p;
+            }
+            if (p < c.max_recv && ro < c.max_recv) {
                 c.recv[p] = rt;
                 c.tile_ctr[p] = 0;
+                c.g1_done[p] = 0;
+                c.rorder[ro] = p;
             } else {
                 s_err = 5;
             }
@@ -608,11 +666,9 @@ void launch_gate_exact(const DevCtx& c, cudaStream_t st) {
 
 // route + permutation + count publish (after the gate logits exist)
 void launch_route(const DevCtx& c, cudaStream_t st) {
-    k_route<<<(c.S + 7) / 8, 256, 0, st>>>(c);
+    k_route<<<(c.S + 7) / 8, 256, 0, st>>>(c);  // + block histograms
     const int nb = (c.S + kPermT - 1) / kPermT;
-    k_hist<<<nb, kPermT, sizeof(int32_t) * c.E, st>>>(c);
-    k_perm<<<nb, kPermT, perm_smem_bytes(c), st>>>(c);
-    k_publish_counts<<<1, 256, 0, st>>>(c);
+    k_perm<<<nb, kPermT, perm_smem_bytes(c), st>>>(c);  // + count publish
 }
 
 size_t perm_smem_bytes(const DevCtx& c) {
@@ -621,11 +677,13 @@ size_t perm_smem_bytes(const DevCtx& c) {
 
 size_t plan_smem_bytes(const DevCtx& c) {
     const size_t PE = size_t(c.P) * c.E;
-    return sizeof(int32_t) * (4 * PE + 2 * size_t(c.E) + 40);
+    return sizeof(int32_t) * (5 * PE + 3 * size_t(c.E) + 48);
 }
 
+void launch_plan(const DevCtx& c, cudaStream_t st) { k_plan<<<1, 1024, plan_smem_bytes(c), st>>>(c); }
+
 void launch_dispatch(const DevCtx& c, cudaStream_t st) {
-    k_plan<<<1, 1024, plan_smem_bytes(c), st>>>(c);
+    launch_plan(c, st);
     k_dispatch<<<c.max_send, 256, 0, st>>>(c);
 }
 

@@ -25,6 +25,10 @@ void launch_gate_exact(const DevCtx& c, cudaStream_t st);
 void launch_gate_tc(const CUtensorMap& tx, const CUtensorMap& twg, const DevCtx& c, int grid, cudaStream_t st);
 void launch_route(const DevCtx& c, cudaStream_t st);
 void launch_dispatch(const DevCtx& c, cudaStream_t st);
+void launch_plan(const DevCtx& c, cudaStream_t st);
+cudaError_t configure_moe();
+cudaError_t launch_moe(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
+                       const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
 void launch_combine(const DevCtx& c, cudaStream_t st);
 cudaError_t configure_kernels(const DevCtx& c);
 size_t gemm_smem_bytes();
@@ -92,6 +96,7 @@ struct perseus_layer {
     int H = 0, I = 0, E = 0, k = 0, S = 0, El = 0;
     int64_t R_max = 0, T_max = 0, Y_rows = 0;
     int max_send = 0, max_recv = 0;
+    int gate_splits = 1, hist_blocks = 1;
     int num_sms = 148;
     uint32_t epoch = 0;
     cudaStream_t stream = nullptr;
@@ -107,6 +112,9 @@ struct perseus_layer {
     Group *groups = nullptr, *cgroups = nullptr;
     RecvTile* recv = nullptr;
     uint32_t *group_ctr = nullptr, *cgroup_ctr = nullptr, *tile_ctr = nullptr;
+    int32_t *sorder = nullptr, *rorder = nullptr;
+    uint32_t *send_done = nullptr, *g1_done = nullptr, *self_ready = nullptr, *sched = nullptr;
+    bool fused = true;  // forward() uses the fused persistent kernel
     unsigned long long* stats = nullptr;
 
     // symmetric region
@@ -135,6 +143,8 @@ struct perseus_layer {
         c.wg = wg; c.logits = logits; c.ids = ids; c.weights = weights; c.counts = counts;
         c.offsets = offsets; c.rows = rows; c.pos = pos; c.zipf_ids = zipf_ids; c.hbuf = hbuf;
         c.hist = hist;
+        c.hist_blocks = hist_blocks;
+        c.gate_splits = gate_splits;
         for (int p = 0; p < world; ++p) {
             uint8_t* b = peer[p];
             c.count_table[p] = reinterpret_cast<int32_t*>(b + off_ctab);
@@ -148,6 +158,8 @@ struct perseus_layer {
         c.hdr = hdr; c.send = send; c.groups = groups; c.recv = recv; c.cgroups = cgroups;
         c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
         c.max_send = max_send; c.max_recv = max_recv;
+        c.sorder = sorder; c.rorder = rorder; c.send_done = send_done; c.g1_done = g1_done;
+        c.self_ready = self_ready; c.sched = sched;
         c.stats = stats;
         return c;
     }
@@ -191,7 +203,8 @@ void free_layer(perseus_layer* L) {
         if (L->ipc_mapped[p]) cudaIpcCloseMemHandle(L->peer[p]);
     void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
-                    L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym};
+                    L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
+                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : L->ev)
@@ -222,6 +235,20 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         launch_route(c, st);
     }
     if (all) ck(cudaEventRecord(L->ev[1], st), "event");
+    if (all && L->fused) {
+        // one persistent kernel: dispatch puts + GEMM1 + GEMM2/combine puts,
+        // overlapped tile by tile (gemm.cu:k_moe)
+        launch_plan(c, st);
+        ck(cudaEventRecord(L->ev[2], st), "event");
+        ck(launch_moe(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
+           "launch k_moe");
+        ck(cudaEventRecord(L->ev[3], st), "event");
+        ck(cudaEventRecord(L->ev[4], st), "event");
+        launch_combine(c, st);
+        ck(cudaEventRecord(L->ev[5], st), "event");
+        ck(cudaGetLastError(), "kernel launch");
+        return;
+    }
     if (all || phase == PERSEUS_PHASE_DISPATCH) launch_dispatch(c, st);
     if (all) ck(cudaEventRecord(L->ev[2], st), "event");
     if (all || phase == PERSEUS_PHASE_EXPERT) {
@@ -249,6 +276,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
         auto* L = new perseus_layer;
         try {
             L->cfg = *cfg;
+            L->fused = !(cfg->flags & PERSEUS_F_UNFUSED);
             L->rank = rank;
             L->world = world;
             L->device = device;
@@ -276,7 +304,9 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->w1 = dalloc<bf16>(El * 2 * I * H);
             L->w2 = dalloc<bf16>(El * H * I);
             L->hbuf = dalloc<bf16>(size_t(L->R_max) * I);
-            L->logits = dalloc<float>(S * E);
+            L->hist_blocks = int((S + 255) / 256);
+            L->gate_splits = (H / 64) % 4 == 0 ? 4 : 1;
+            L->logits = dalloc<float>(size_t(L->gate_splits) * S * E);
             L->weights = dalloc<float>(Sk);
             L->ids = dalloc<int32_t>(Sk);
             L->counts = dalloc<int32_t>(E);
@@ -284,7 +314,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->rows = dalloc<int32_t>(Sk);
             L->pos = dalloc<int32_t>(Sk);
             L->zipf_ids = dalloc<int32_t>(Sk);
-            L->hist = dalloc<int32_t>(((S + 255) / 256) * E);
+            L->hist = dalloc<int32_t>(2 * size_t(L->hist_blocks) * E);
             L->hdr = dalloc<PlanHeader>(1);
             L->send = dalloc<SendTile>(L->max_send);
             L->groups = dalloc<Group>(L->max_send);
@@ -293,6 +323,12 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->group_ctr = dalloc<uint32_t>(L->max_send);
             L->cgroup_ctr = dalloc<uint32_t>(L->max_recv);
             L->tile_ctr = dalloc<uint32_t>(L->max_recv);
+            L->sorder = dalloc<int32_t>(L->max_send);
+            L->rorder = dalloc<int32_t>(L->max_recv);
+            L->send_done = dalloc<uint32_t>(L->max_send);
+            L->g1_done = dalloc<uint32_t>(L->max_recv);
+            L->self_ready = dalloc<uint32_t>(L->max_recv);
+            L->sched = dalloc<uint32_t>(4);
             L->stats = dalloc<unsigned long long>(kStatCount);
 
             // symmetric region: identical layout on every rank
@@ -318,6 +354,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->tm_b2 = make_tmap(L->w2, El * H, I);
             L->tm_wg = make_tmap(L->wg, E, H);
             ck(configure_gemm(), "configure_gemm");
+            ck(configure_moe(), "configure_moe");
             ck(configure_kernels(L->ctx(nullptr, nullptr)), "configure_kernels");
             if (world == 1) {
                 L->peer[0] = L->sym;

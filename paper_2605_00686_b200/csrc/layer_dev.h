@@ -31,7 +31,9 @@ struct DevCtx {
     int32_t* offsets;    // [E+1]: sorted segment starts of this rank's (token, j) pairs
     int32_t* rows;       // [S*k]: token of each sorted slot
     int32_t* pos;        // [S*k]: sorted slot of each (token, j)
-    int32_t* hist;       // [ceil(S/256)][E]: per-block expert histogram
+    int32_t* hist;       // [2][hist_blocks][E]: per-256-token-block expert histogram (parity halves)
+    int32_t hist_blocks; // ceil(S/256)
+    int32_t gate_splits; // tensor-core router: K splits, logits = sum of [gate_splits][S][E] partials
     const int32_t* zipf_ids;  // [S*k]: reference Zipf draws (routing == ZIPF)
     bf16* hbuf;          // [R_max][I]
 
@@ -54,6 +56,13 @@ struct DevCtx {
     uint32_t* cgroup_ctr;
     uint32_t* tile_ctr;
     int32_t max_send, max_recv;
+    // fused-kernel scheduling (rebuilt by k_plan every forward)
+    int32_t* sorder;      // [max_send]: send positions in copy order (dst-interleaved)
+    int32_t* rorder;      // [max_recv]: recv positions in processing order (self, then by arrival)
+    uint32_t* send_done;  // [max_send]: rows copied per send tile
+    uint32_t* g1_done;    // [max_recv]: GEMM1 n-blocks finished per M-tile
+    uint32_t* self_ready; // [max_recv]: epoch when a self tile's rows are in the heap
+    uint32_t* sched;      // [4]: work-item / copy-unit counters
 
     unsigned long long* stats;  // [kStatCount]
 };

@@ -47,6 +47,8 @@ struct SendTile {
     int64_t heap_row;  // first destination row in dst's receive heap
     int32_t tile_id;   // reference tile id == flag word id (-1: self segment)
     int32_t group;     // signal group (-1: self segment, no signal)
+    int32_t recv_pos;  // self segment: position of the matching RecvTile (else -1)
+    int32_t pad;
 };
 
 // Signal group: members are a contiguous run of the tile list in the

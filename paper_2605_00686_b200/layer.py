@@ -40,14 +40,17 @@ def _stream(stream) -> Optional[int]:
 class MoELayer:
     def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
                  device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
-                 protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True):
+                 protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True,
+                 fused: bool = True):
         protocol = protocol or combined_protocol(0)
+        self.fused = fused
         self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
         self.routing_mode, self.skew, self.seed, self.protocol = routing, skew, seed, protocol
         cfg = _lib.LayerConfig(model.hidden_dim, model.intermediate_dim, model.experts, model.top_k,
                                tokens_per_pe, ROUTING[routing], float(skew), seed,
                                protocol.device_signaling(), protocol.group_size,
-                               _lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
+                               (_lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
+                               | (0 if fused else _lib.F_UNFUSED))
         self._cfg = cfg
         h = C.c_void_p()
         check(lib.perseus_layer_create(C.byref(cfg), rank, world, device, C.byref(h)))
