@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
         } else {
             hrow = rows_in_r + selfo[j];
         }
+        c.send_first[e] = pos0;
         for (int ch = 0; ch < nt; ++ch) {
             SendTile st;
             st.expert = e;
@@ -618,43 +619,50 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
 // --------------------------------------------------------------- combine ----
 // Wait for every combine tile this rank dispatched to come back, then
 // out[t] = sum_j w[t][j] * y[pos(t, j)] in fixed j order (fp32) -> bf16.
-__global__ void __launch_bounds__(256) k_combine(DevCtx c) {
-    const PlanHeader hdr = *c.hdr;
-    if (c.P > 1 && threadIdx.x < 32) {
-        const uint32_t* flags = c.cflag[c.rank] + size_t(c.par) * c.T_max;
-        for (int q = threadIdx.x; q < hdr.n_send_remote; q += 32) {
-            const int tile = c.send[q].tile_id;
-            if (!wait_flag_geq(flags + tile, c.epoch, kWaitTimeoutNs))
+// One CTA per token, one thread per 16-byte column chunk.  Only the (at most
+// k) combine tiles that carry this token's rows are waited on — the tile of
+// sorted slot p is send tile send_first[e] + (p - offsets[e]) / 128.
+template <int K>
+__global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
+    const int t = blockIdx.x, v = threadIdx.x;
+    const int k = K > 0 ? K : c.k;
+    if (c.P > 1 && v < k) {
+        const int e = c.ids[size_t(t) * k + v];
+        if (e % c.P != c.rank) {
+            const int32_t rel = c.pos[size_t(t) * k + v] - c.offsets[e];
+            const int tile = c.send[c.send_first[e] + rel / kTileRows].tile_id;
+            if (!wait_flag_geq(c.cflag[c.rank] + size_t(c.par) * c.T_max + tile, c.epoch, kWaitTimeoutNs))
                 atomicAdd(&c.stats[kStatTimeouts], 1ull);
         }
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (t >= c.S) return;
     const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
-    int32_t p[16];
-    float w[16];
-    for (int j = 0; j < c.k; ++j) {
-        p[j] = c.pos[size_t(t) * c.k + j];
-        w[j] = c.weights[size_t(t) * c.k + j];
+    constexpr int KM = K > 0 ? K : 16;
+    uint4 u[KM];
+    float w[KM];
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+        if (j < k) {
+            const int32_t p = c.pos[size_t(t) * k + j];
+            w[j] = c.weights[size_t(t) * k + j];
+            u[j] = *reinterpret_cast<const uint4*>(y + size_t(p) * c.H + v * 8);
+        }
     }
-    const int nvec = c.H / 8;
-    for (int v = lane; v < nvec; v += 32) {
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int j = 0; j < c.k; ++j) {
-            const uint4 u = *reinterpret_cast<const uint4*>(y + size_t(p[j]) * c.H + v * 8);
-            const bf16* b = reinterpret_cast<const bf16*>(&u);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+        if (j < k) {
+            const bf16* b = reinterpret_cast<const bf16*>(&u[j]);
 #pragma unroll
             for (int q = 0; q < 8; ++q) acc[q] = __fmaf_rn(w[j], __bfloat162float(b[q]), acc[q]);
         }
-        uint4 o;
-        o.x = pack_bf16(acc[0], acc[1]);
-        o.y = pack_bf16(acc[2], acc[3]);
-        o.z = pack_bf16(acc[4], acc[5]);
-        o.w = pack_bf16(acc[6], acc[7]);
-        *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + v * 8) = o;
     }
+    uint4 o;
+    o.x = pack_bf16(acc[0], acc[1]);
+    o.y = pack_bf16(acc[2], acc[3]);
+    o.z = pack_bf16(acc[4], acc[5]);
+    o.w = pack_bf16(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + v * 8) = o;
 }
 
 // ------------------------------------------------------------- launchers ----
@@ -688,7 +696,14 @@ void launch_dispatch(const DevCtx& c, cudaStream_t st) {
 }
 
 void launch_combine(const DevCtx& c, cudaStream_t st) {
-    k_combine<<<(c.S + 7) / 8, 256, 0, st>>>(c);
+    const int threads = c.H / 8;  // H <= 8192
+    switch (c.k) {
+        case 1: k_combine<1><<<c.S, threads, 0, st>>>(c); break;
+        case 2: k_combine<2><<<c.S, threads, 0, st>>>(c); break;
+        case 4: k_combine<4><<<c.S, threads, 0, st>>>(c); break;
+        case 8: k_combine<8><<<c.S, threads, 0, st>>>(c); break;
+        default: k_combine<0><<<c.S, threads, 0, st>>>(c); break;
+    }
 }
 
 cudaError_t configure_kernels(const DevCtx& c) {

@@ -114,6 +114,7 @@ struct perseus_layer {
     uint32_t *group_ctr = nullptr, *cgroup_ctr = nullptr, *tile_ctr = nullptr;
     int32_t *sorder = nullptr, *rorder = nullptr;
     uint32_t *send_done = nullptr, *g1_done = nullptr, *self_ready = nullptr, *sched = nullptr;
+    int32_t* send_first = nullptr;
     bool fused = true;  // forward() uses the fused persistent kernel
     unsigned long long* stats = nullptr;
 
@@ -159,7 +160,7 @@ struct perseus_layer {
         c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
         c.max_send = max_send; c.max_recv = max_recv;
         c.sorder = sorder; c.rorder = rorder; c.send_done = send_done; c.g1_done = g1_done;
-        c.self_ready = self_ready; c.sched = sched;
+        c.self_ready = self_ready; c.sched = sched; c.send_first = send_first;
         c.stats = stats;
         return c;
     }
@@ -174,6 +175,7 @@ void validate(const perseus_layer_config& c, int rank, int world) {
     if (rank < 0 || rank >= world) throw sigsim::ConfigError("rank out of range");
     if (c.experts % world) throw sigsim::ConfigError("experts not divisible by PEs");
     if (c.hidden_dim % 256) throw sigsim::ConfigError("hidden_dim must be a multiple of 256");
+    if (c.hidden_dim > 8192) throw sigsim::ConfigError("hidden_dim must be <= 8192");
     if (c.intermediate_dim % 128) throw sigsim::ConfigError("intermediate_dim must be a multiple of 128");
     if (c.experts > 256) throw sigsim::ConfigError("experts must be <= 256");
     if (c.top_k > 16) throw sigsim::ConfigError("top_k must be <= 16");
@@ -204,7 +206,8 @@ void free_layer(perseus_layer* L) {
     void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
-                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched};
+                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched,
+                    L->send_first};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : L->ev)
@@ -329,6 +332,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->g1_done = dalloc<uint32_t>(L->max_recv);
             L->self_ready = dalloc<uint32_t>(L->max_recv);
             L->sched = dalloc<uint32_t>(4);
+            L->send_first = dalloc<int32_t>(E);
             L->stats = dalloc<unsigned long long>(kStatCount);
 
             // symmetric region: identical layout on every rank

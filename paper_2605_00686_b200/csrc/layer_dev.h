@@ -63,6 +63,7 @@ struct DevCtx {
     uint32_t* g1_done;    // [max_recv]: GEMM1 n-blocks finished per M-tile
     uint32_t* self_ready; // [max_recv]: epoch when a self tile's rows are in the heap
     uint32_t* sched;      // [4]: work-item / copy-unit counters
+    int32_t* send_first;  // [E]: first send position of each expert's tiles
 
     unsigned long long* stats;  // [kStatCount]
 };
