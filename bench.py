@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="stage kernels instead of the fused persistent kernel")
+    ap.add_argument("--no-pair", action="store_true", help="fused kernel on single CTAs instead of CTA pairs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3  # timing rule: W >= 3
@@ -236,7 +237,8 @@ def main():
     proto = {"combined": pb.combined_protocol(0), "vanilla": pb.vanilla_protocol(),
              "decoupled": pb.decoupled_protocol(0)}[args.signaling]
     layer = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing,
-                        skew=args.skew, seed=1, protocol=proto, fused=not args.unfused)
+                        skew=args.skew, seed=1, protocol=proto, fused=not args.unfused,
+                        pair=not args.no_pair)
     if world > 1:
         layer.connect_dist()
     stream = torch.cuda.current_stream()
@@ -357,6 +359,7 @@ def main():
                                  ["route_permute", "plan", "fused_dispatch_ffn_combineput", "-", "combine"],
                                  st_mean)),
             "fused": not args.unfused,
+            "cta_pairs": not args.no_pair and not args.unfused,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes},
             "roofline": roof,

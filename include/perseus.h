@@ -126,6 +126,7 @@ typedef struct perseus_layer_config {
 
 #define PERSEUS_F_SYNTH_WEIGHTS 1 /* generate weights on device from `seed` */
 #define PERSEUS_F_UNFUSED 2       /* forward() as stream-ordered stage kernels instead of the fused persistent kernel */
+#define PERSEUS_F_NO_PAIR 4       /* fused kernel on single CTAs (cta_group::1) instead of CTA pairs (cta_group::2) */
 
 /* Tile granularity: 128 token rows per transfer tile / GEMM M-tile, i.e. the
  * reference's tile_bytes = 128 * H * 2 (workload.hpp:58). */

@@ -17,6 +17,7 @@ SIGNAL_COUPLED, SIGNAL_DECOUPLED, SIGNAL_NONE = 0, 1, 2
 PHASE_ROUTE, PHASE_DISPATCH, PHASE_EXPERT, PHASE_COMBINE, PHASE_ALL = 0, 1, 2, 3, 15
 F_SYNTH_WEIGHTS = 1
 F_UNFUSED = 2
+F_NO_PAIR = 4
 TILE_ROWS = 128
 
 

@@ -323,6 +323,8 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
     int32_t* scratch = rp + E;    // 33 (+pad)
     int32_t* selfo = scratch + 40;  // [El] self-segment row offsets
     int32_t* tb2 = selfo + El;      // [P*E] scratch
+    int32_t* ppos = tb2 + PE;       // [E] pair position per (ks, j)
+    __shared__ int32_t src_pfirst[kMaxPes], src_np[kMaxPes];
     __shared__ int32_t s_err;
     __shared__ int32_t dst_first[kMaxPes + 1], dst_group[kMaxPes], src_first[kMaxPes + 1],
         src_group[kMaxPes], dst_n[kMaxPes], src_n[kMaxPes];
@@ -554,6 +556,46 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
         c.cgroups[src_group[s]] = G;
         c.cgroup_ctr[src_group[s]] = 0;
     }
+    // ---- M-tile pairs for the CTA-pair (cta_group::2) kernel: consecutive
+    // chunks of one (src, expert) segment share the expert's weights; an odd
+    // last chunk is paired with nothing (-1).  Pair order mirrors rorder.
+    for (int i = tid; i < P * El; i += 1024) {
+        const int s = i / El, j = i % El;
+        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+        ppos[ks * El + j] = (ceil_tiles(T[s * E + r + P * j]) + 1) / 2;
+    }
+    __syncthreads();
+    const int32_t n_pairs = block_exclusive_scan(ppos, P * El, scratch);
+    if (tid == 0) {
+        for (int ks = 0; ks < P; ++ks) {
+            const int s = ks == 0 ? r : (ks <= r ? ks - 1 : ks);
+            const int first = ppos[ks * El];
+            src_pfirst[s] = first;
+            src_np[s] = (ks + 1 < P ? ppos[(ks + 1) * El] : n_pairs) - first;
+        }
+    }
+    __syncthreads();
+    const int32_t n_pairs_self = src_np[r];
+    for (int i = tid; i < P * El; i += 1024) {
+        const int s = i / El, j = i % El;
+        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+        const int nt = ceil_tiles(T[s * E + r + P * j]);
+        const int32_t pos0 = rp[ks * El + j];
+        for (int pi = 0; 2 * pi < nt; ++pi) {
+            const int q = ppos[ks * El + j] + pi;
+            int po = q;
+            if (s != r) {
+                const int idx = q - src_pfirst[s];
+                po = n_pairs_self;
+                for (int z = 0; z < P; ++z)
+                    if (z != r) po += min(src_np[z], idx) + ((z < s && src_np[z] > idx) ? 1 : 0);
+            }
+            if (po < c.max_recv) {
+                c.pairs[2 * po] = pos0 + 2 * pi;
+                c.pairs[2 * po + 1] = 2 * pi + 1 < nt ? pos0 + 2 * pi + 1 : -1;
+            }
+        }
+    }
     __syncthreads();
     if (tid == 0) {
         PlanHeader h;
@@ -565,6 +607,8 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
         h.n_cgroups = n_cgroups;
         h.total_tiles = total_tiles;
         h.error = s_err;
+        h.n_pairs = n_pairs;
+        h.pad = 0;
         h.remote_rows_in = rows_in_r;
         *c.hdr = h;
         if (s_err) atomicAdd(&c.stats[kStatErrors], 1ull);
@@ -685,7 +729,7 @@ size_t perm_smem_bytes(const DevCtx& c) {
 
 size_t plan_smem_bytes(const DevCtx& c) {
     const size_t PE = size_t(c.P) * c.E;
-    return sizeof(int32_t) * (5 * PE + 3 * size_t(c.E) + 48);
+    return sizeof(int32_t) * (5 * PE + 4 * size_t(c.E) + 48);
 }
 
 void launch_plan(const DevCtx& c, cudaStream_t st) { k_plan<<<1, 1024, plan_smem_bytes(c), st>>>(c); }

@@ -27,6 +27,9 @@ void launch_route(const DevCtx& c, cudaStream_t st);
 void launch_dispatch(const DevCtx& c, cudaStream_t st);
 void launch_plan(const DevCtx& c, cudaStream_t st);
 cudaError_t configure_moe();
+cudaError_t configure_moe2();
+cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
+                        const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
 cudaError_t launch_moe(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
                        const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
 void launch_combine(const DevCtx& c, cudaStream_t st);
@@ -116,6 +119,8 @@ struct perseus_layer {
     uint32_t *send_done = nullptr, *g1_done = nullptr, *self_ready = nullptr, *sched = nullptr;
     int32_t* send_first = nullptr;
     bool fused = true;  // forward() uses the fused persistent kernel
+    bool pair = true;   // ... on CTA pairs (cta_group::2)
+    int32_t* pairs = nullptr;
     unsigned long long* stats = nullptr;
 
     // symmetric region
@@ -160,7 +165,7 @@ struct perseus_layer {
         c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
         c.max_send = max_send; c.max_recv = max_recv;
         c.sorder = sorder; c.rorder = rorder; c.send_done = send_done; c.g1_done = g1_done;
-        c.self_ready = self_ready; c.sched = sched; c.send_first = send_first;
+        c.self_ready = self_ready; c.sched = sched; c.send_first = send_first; c.pairs = pairs;
         c.stats = stats;
         return c;
     }
@@ -207,7 +212,7 @@ void free_layer(perseus_layer* L) {
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
                     L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched,
-                    L->send_first};
+                    L->send_first, L->pairs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : L->ev)
@@ -243,8 +248,12 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         // overlapped tile by tile (gemm.cu:k_moe)
         launch_plan(c, st);
         ck(cudaEventRecord(L->ev[2], st), "event");
-        ck(launch_moe(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
-           "launch k_moe");
+        if (L->pair)
+            ck(launch_moe2(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
+               "launch k_moe2");
+        else
+            ck(launch_moe(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
+               "launch k_moe");
         ck(cudaEventRecord(L->ev[3], st), "event");
         ck(cudaEventRecord(L->ev[4], st), "event");
         launch_combine(c, st);
@@ -280,6 +289,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
         try {
             L->cfg = *cfg;
             L->fused = !(cfg->flags & PERSEUS_F_UNFUSED);
+            L->pair = !(cfg->flags & PERSEUS_F_NO_PAIR);
             L->rank = rank;
             L->world = world;
             L->device = device;
@@ -333,6 +343,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->self_ready = dalloc<uint32_t>(L->max_recv);
             L->sched = dalloc<uint32_t>(4);
             L->send_first = dalloc<int32_t>(E);
+            L->pairs = dalloc<int32_t>(2 * size_t(L->max_recv) + 4);
             L->stats = dalloc<unsigned long long>(kStatCount);
 
             // symmetric region: identical layout on every rank
@@ -359,6 +370,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->tm_wg = make_tmap(L->wg, E, H);
             ck(configure_gemm(), "configure_gemm");
             ck(configure_moe(), "configure_moe");
+            ck(configure_moe2(), "configure_moe2");
             ck(configure_kernels(L->ctx(nullptr, nullptr)), "configure_kernels");
             if (world == 1) {
                 L->peer[0] = L->sym;

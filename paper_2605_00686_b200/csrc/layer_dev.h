@@ -64,6 +64,7 @@ struct DevCtx {
     uint32_t* self_ready; // [max_recv]: epoch when a self tile's rows are in the heap
     uint32_t* sched;      // [4]: work-item / copy-unit counters
     int32_t* send_first;  // [E]: first send position of each expert's tiles
+    int32_t* pairs;       // [max_recv][2]: M-tile pairs (recv positions, -1 = none) in processing order
 
     unsigned long long* stats;  // [kStatCount]
 };

@@ -1,0 +1,465 @@
+// moe2.cu — the fused forward on CTA PAIRS (tcgen05 cta_group::2).
+//
+// Same structure as k_moe (gemm.cu): copy warps stream dispatch units, a
+// scheduler + TMA producer, one MMA thread, four epilogue warps — but each
+// work item is a PAIR of M-tiles of the same expert (consecutive chunks of a
+// (src, expert) segment) computed as ONE 256 x 256 UMMA tile by two CTAs of a
+// cluster:
+//   * each CTA loads its own 128 A rows and HALF of the B tile (GEMM1: CTA0
+//     the gate rows, CTA1 the up rows; GEMM2: the two 128-row halves of W2's
+//     256-row n-block), so every weight byte crosses L2->SM once per pair
+//     instead of once per M-tile: 32 KB/stage/CTA instead of 48 KB.  At EP=1
+//     the L2->SM bandwidth (not HBM, not the tensor pipe) caps the 1-CTA
+//     kernel near 45% tensor utilisation; this removes a third of that traffic;
+//   * the leader CTA (cluster rank 0) grabs work items, mirrors them into its
+//     peer's ring through DSMEM, and issues tcgen05.mma.cta_group::2; the
+//     peer's TMA bytes complete on the leader's full barrier; MMA completion
+//     is committed to both CTAs' barriers (multicast); both CTAs' epilogues
+//     release the leader's TMEM-empty barrier.
+// An odd last chunk is paired with nothing: the peer recomputes its partner's
+// rows and discards them.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "layer_dev.h"
+#include "perseus.h"
+#include "ptx.cuh"
+#include "signal.cuh"
+
+namespace perseus {
+namespace {
+
+using namespace ptx;
+
+constexpr int kStages = 6;
+constexpr int kBM = 128, kBN = 256, kBK = 64;
+constexpr int kA = kBM * kBK * 2;         // 16 KB: this CTA's A rows
+constexpr int kBh = 128 * kBK * 2;        // 16 KB: this CTA's half of B
+constexpr int kStage = kA + kBh;          // 32 KB
+constexpr int kTmemCols = 512;
+constexpr int kStgRow = 128 + 16;
+constexpr int kStgBytes = 128 * kStgRow;
+constexpr int kRing = 8;
+constexpr int kUnitRows = 16;
+constexpr int kUnitsPerTile = kTileRows / kUnitRows;
+constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
+
+struct Args {
+    int32_t n1, n2, kb1, kb2, lag, pad;
+    int64_t a1_row_base;
+};
+struct Item {
+    int32_t kind, t, nb;
+};
+
+__device__ __forceinline__ Item item_of(int w, int T, const Args& f) {
+    const int L = min(f.lag, T), n1 = f.n1, n2 = f.n2;
+    if (w < L * n1) return {1, w / n1, w % n1};
+    w -= L * n1;
+    const int steady = (T - L) * (n1 + n2);
+    if (w < steady) {
+        const int st = w / (n1 + n2), r = w % (n1 + n2);
+        return r < n1 ? Item{1, L + st, r} : Item{2, st, r - n1};
+    }
+    w -= steady;
+    if (w < L * n2) return {2, T - L + w / n2, w % n2};
+    return {0, 0, 0};
+}
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
+
+__device__ __forceinline__ void copy_unit(const DevCtx& c, const SendTile& st, int r0, int nrows, int lane) {
+    const int32_t abs0 = c.offsets[st.expert] + st.row0 + r0;
+    bf16* dbase = c.heap[st.dst] + (size_t(c.par) * c.R_max + st.heap_row + r0) * c.H;
+    const int nvec = c.H / 8;
+    for (int rr = 0; rr < nrows; ++rr) {
+        const int32_t tok = c.rows[abs0 + rr];
+        const uint4* src = reinterpret_cast<const uint4*>(c.x + size_t(tok) * c.H);
+        uint4* dst = reinterpret_cast<uint4*>(dbase + size_t(rr) * c.H);
+        int v = lane;
+        for (; v + 224 < nvec; v += 256) {
+            uint4 a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = __ldg(src + v + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dst[v + 32 * u] = a[u];
+        }
+        for (; v < nvec; v += 32) dst[v] = __ldg(src + v);
+    }
+}
+
+// combine-direction completion of one n-block of a remote M-tile (4 epilogue warps)
+__device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, int nb) {
+    named_bar_sync(1, 128);
+    if ((threadIdx.x >> 5) != 4) return;
+    const int lane = threadIdx.x & 31;
+    const RecvTile rt = c.recv[ti];
+    if (lane == 0 && nb == 0) atomicAdd(&c.stats[kStatRecvTiles], 1ull);
+    if (rt.cgroup < 0) return;
+    uint32_t done = 0;
+    if (lane == 0) done = atom_add_acq_rel_gpu(c.tile_ctr + ti, 1u) + 1 == uint32_t(n_nb);
+    if (!__shfl_sync(0xffffffffu, done, 0)) return;
+    if (lane == 0) {
+        atomicAdd(&c.stats[kStatCombinePuts], 1ull);
+        atomicAdd(&c.stats[kStatCombineBytes], (unsigned long long)rt.rows * c.H * 2);
+    }
+    const Group grp = c.cgroups[rt.cgroup];
+    auto flag_of = [&](int m) {
+        const RecvTile& mt = c.recv[m];
+        return c.cflag[mt.src] + size_t(c.par) * c.T_max + mt.tile_id;
+    };
+    publish_member_warp(c, grp, c.cgroup_ctr + rt.cgroup, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+                        kStatCombineFences, kStatCombineSignals);
+}
+
+__device__ __forceinline__ uint32_t pk(const uint32_t* v, int i) {
+    return pack_bf16(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+}
+
+}  // namespace
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    k_moe2(const __grid_constant__ CUtensorMap tm_a1, const __grid_constant__ CUtensorMap tm_b1,
+           const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b2, DevCtx c,
+           Args f) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stage_out = smem + kStages * kStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + kStgBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* rfull = tempty + 2;
+    uint64_t* rempty = rfull + kRing;
+    int32_t* ring = reinterpret_cast<int32_t*>(rempty + kRing);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ring + kRing);
+
+    const PlanHeader hdr = *c.hdr;  // identical in both CTAs: they return together
+    if (hdr.error) return;
+    const int T = hdr.n_pairs;
+    const int total = T * (f.n1 + f.n2);
+    const int warp = warp_id(), lane = lane_id();
+    const uint32_t crank = cluster_ctarank();
+    const bool lead = crank == 0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_a1);
+        tma_prefetch_desc(&tm_b1);
+        tma_prefetch_desc(&tm_a2);
+        tma_prefetch_desc(&tm_b2);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the live one)
+        }
+        for (int s = 0; s < kRing; ++s) {
+            mbar_init(&rfull[s], 1);
+            mbar_init(&rempty[s], 10);  // leader: MMA + 4 epi; peer: producer + 4 epi
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        tmem_alloc_pair(tmem_holder, kTmemCols);
+        tmem_relinquish_pair();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- scheduler (leader) + TMA producer (both) ----------------
+            int stage = 0, slot = 0;
+            uint32_t phase = 0, rphase = 0;
+            const uint32_t* dflags = c.dflag[c.rank] + size_t(c.par) * c.T_max;
+            while (true) {
+                int w;
+                if (lead) {
+                    w = int(atomicAdd(&c.sched[0], 1u));
+                    if (w >= total) w = -1;
+                    mbar_wait(&rempty[slot], rphase ^ 1);
+                    ring[slot] = w;
+                    mbar_arrive(&rfull[slot]);
+                    st_cluster_u32(mapa(smem_u32(&ring[slot]), 1), uint32_t(w));
+                    mbar_arrive_cluster(mapa(smem_u32(&rfull[slot]), 1));
+                } else {
+                    mbar_wait(&rfull[slot], rphase);
+                    w = ring[slot];
+                    mbar_arrive_cluster(mapa(smem_u32(&rempty[slot]), 0));
+                }
+                if (++slot == kRing) { slot = 0; rphase ^= 1; }
+                if (w < 0) break;
+                const Item it = item_of(w, T, f);
+                const int t0 = c.pairs[2 * it.t], t1 = c.pairs[2 * it.t + 1];
+                const int mine = (crank == 0 || t1 < 0) ? t0 : t1;
+                const RecvTile rt = c.recv[mine];
+                int32_t a_row, b_row, nkb;
+                const CUtensorMap* ta;
+                const CUtensorMap* tb;
+                if (it.kind == 1) {
+                    const bool ok = rt.tile_id >= 0 ? wait_flag_geq(dflags + rt.tile_id, c.epoch, kWaitTimeoutNs)
+                                                    : wait_flag_geq(c.self_ready + mine, c.epoch, kWaitTimeoutNs);
+                    if (!ok) atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                    a_row = int32_t(f.a1_row_base + rt.heap_row);
+                    b_row = rt.e_local * 2 * c.I + it.nb * 128 + (crank ? c.I : 0);  // gate | up
+                    nkb = f.kb1;
+                    ta = &tm_a1;
+                    tb = &tm_b1;
+                } else {
+                    if (!wait_flag_geq(c.g1_done + mine, uint32_t(f.n1), kWaitTimeoutNs))
+                        atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                    a_row = int32_t(rt.heap_row);
+                    b_row = rt.e_local * c.H + it.nb * 256 + int(crank) * 128;
+                    nkb = f.kb2;
+                    ta = &tm_a2;
+                    tb = &tm_b2;
+                }
+                fence_proxy_async();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    uint8_t* sa = smem + stage * kStage;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (lead) mbar_arrive_expect_tx(&full[stage], 2 * kStage);
+                    const uint32_t fb = mapa(smem_u32(&full[stage]), 0);
+                    tma_load_2d_pair(sa, ta, fb, kb * kBK, a_row);
+                    tma_load_2d_pair(sa + kA, tb, fb, kb * kBK, b_row);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && lead) {
+            // ---------------- MMA issuer (leader CTA) ----------------
+            const uint32_t idesc = idesc_bf16_f32(2 * kBM, kBN);
+            int stage = 0, slot = 0, acc = 0;
+            uint32_t phase = 0, rphase = 0, aphase = 0;
+            while (true) {
+                mbar_wait(&rfull[slot], rphase);
+                const int w = ring[slot];
+                mbar_arrive(&rempty[slot]);
+                if (++slot == kRing) { slot = 0; rphase ^= 1; }
+                if (w < 0) break;
+                const Item it = item_of(w, T, f);
+                const int nkb = it.kind == 1 ? f.kb1 : f.kb2;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * kBN);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    uint8_t* sa = smem + stage * kStage;
+                    const uint64_t adesc = smem_desc_sw128(sa);
+                    const uint64_t bdesc = smem_desc_sw128(sa + kA);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk)
+                        umma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+                    umma_commit_pair(&empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                umma_commit_pair(&tfull[acc]);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else if (warp < 4) {
+        // ---------------- copy warps: dispatch puts ----------------
+        const int total_units = hdr.n_send * kUnitsPerTile;
+        while (true) {
+            int u = 0;
+            if (lane == 0) u = int(atomicAdd(&c.sched[1], 1u));
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u >= total_units) break;
+            const int sp = c.sorder[u / kUnitsPerTile];
+            const SendTile st = c.send[sp];
+            const int r0 = (u % kUnitsPerTile) * kUnitRows;
+            if (r0 >= st.rows) continue;
+            const int nrows = min(kUnitRows, st.rows - r0);
+            copy_unit(c, st, r0, nrows, lane);
+            __syncwarp();
+            uint32_t done = 0;
+            if (lane == 0) done = atom_add_acq_rel_gpu(c.send_done + sp, uint32_t(nrows)) + nrows == uint32_t(st.rows);
+            if (!__shfl_sync(0xffffffffu, done, 0)) continue;
+            if (st.dst == c.rank) {
+                if (lane == 0) st_release_gpu(c.self_ready + st.recv_pos, c.epoch);
+                continue;
+            }
+            if (lane == 0) {
+                atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
+                atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
+            }
+            const Group g = c.groups[st.group];
+            auto flag_of = [&](int m) {
+                const SendTile& t = c.send[m];
+                return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
+            };
+            publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+                                kStatDispatchFences, kStatDispatchSignals);
+        }
+    } else {
+        // ---------------- epilogue (4 warps, this CTA's 128 accumulator rows) ----------------
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        int acc = 0, slot = 0;
+        uint32_t aphase = 0, rphase = 0;
+        int pend_ti = -1, pend_nb = 0;
+        const uint32_t tempty_lead = mapa(smem_u32(&tempty[0]), 0);
+        const uint32_t rempty_lead = mapa(smem_u32(&rempty[0]), 0);
+        while (true) {
+            mbar_wait(&rfull[slot], rphase);
+            const int w = ring[slot];
+            __syncwarp();
+            if (lane == 0) {
+                if (lead) mbar_arrive(&rempty[slot]);
+                else mbar_arrive_cluster(rempty_lead + 8u * slot);
+            }
+            if (++slot == kRing) { slot = 0; rphase ^= 1; }
+            if (w < 0) break;
+            const Item it = item_of(w, T, f);
+            const int t0 = c.pairs[2 * it.t], t1 = c.pairs[2 * it.t + 1];
+            const int mine = crank == 0 ? t0 : t1;  // -1: padding half of an odd pair
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kBN);
+            RecvTile rt;
+            if (mine >= 0) rt = c.recv[mine];
+            const bool valid = mine >= 0 && row < rt.rows;
+            if (it.kind == 1) {
+                if (mine >= 0) {
+                    bf16* dst = c.hbuf + size_t(rt.heap_row + row) * c.I + it.nb * 128;
+#pragma unroll 1
+                    for (int cc = 0; cc < 128; cc += 32) {
+                        uint32_t gv[32], uv[32];
+                        tmem_ld_32x32b_x32(taddr + cc, gv);
+                        tmem_ld_32x32b_x32(taddr + 128 + cc, uv);
+                        tmem_ld_wait();
+                        uint32_t o[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            o[i] = pack_bf16(silu_mul(__uint_as_float(gv[2 * i]), __uint_as_float(uv[2 * i])),
+                                             silu_mul(__uint_as_float(gv[2 * i + 1]), __uint_as_float(uv[2 * i + 1])));
+                        if (valid) {
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) st_global_v4(dst + cc + v * 8, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (lead) mbar_arrive(&tempty[acc]);
+                    else mbar_arrive_cluster(tempty_lead + 8u * acc);
+                }
+                if (mine >= 0) {
+                    named_bar_sync(2, 128);
+                    if (threadIdx.x == 128) atom_add_acq_rel_gpu(c.g1_done + mine, 1u);
+                }
+            } else {
+                if (mine >= 0) {
+                    bf16* dst = c.ybuf[rt.src] + (size_t(c.par) * c.Y_rows + size_t(rt.ybuf_row + row)) * c.H + it.nb * 256;
+                    if (rt.src == c.rank) {
+#pragma unroll 1
+                        for (int cc = 0; cc < 256; cc += 32) {
+                            uint32_t v32[32];
+                            tmem_ld_32x32b_x32(taddr + cc, v32);
+                            tmem_ld_wait();
+                            if (valid) {
+#pragma unroll
+                                for (int v = 0; v < 4; ++v)
+                                    st_global_v4(dst + cc + v * 8, pk(v32, 8 * v), pk(v32, 8 * v + 2), pk(v32, 8 * v + 4), pk(v32, 8 * v + 6));
+                            }
+                        }
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) bulk_commit();
+                    } else {
+                        uint8_t* srow_p = stage_out + (q * 32 + lane) * kStgRow;
+                        const uint32_t srow = smem_u32(srow_p);
+#pragma unroll 1
+                        for (int cc = 0; cc < 256; cc += 64) {
+                            uint32_t v0[32], v1[32];
+                            tmem_ld_32x32b_x32(taddr + cc, v0);
+                            tmem_ld_32x32b_x32(taddr + cc + 32, v1);
+                            tmem_ld_wait();
+                            bulk_wait_read0();
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                st_shared_v4(srow + v * 16, pk(v0, 8 * v), pk(v0, 8 * v + 2), pk(v0, 8 * v + 4), pk(v0, 8 * v + 6));
+                                st_shared_v4(srow + 64 + v * 16, pk(v1, 8 * v), pk(v1, 8 * v + 2), pk(v1, 8 * v + 4), pk(v1, 8 * v + 6));
+                            }
+                            fence_proxy_async_smem();
+                            if (valid) bulk_store(dst + cc, srow_p, 128);
+                            bulk_commit();
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) bulk_commit();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (lead) mbar_arrive(&tempty[acc]);
+                    else mbar_arrive_cluster(tempty_lead + 8u * acc);
+                }
+                if (pend_ti >= 0) {
+                    bulk_wait<4>();
+                    fence_proxy_async();
+                    finish_tile(c, f.n2, pend_ti, pend_nb);
+                }
+                pend_ti = mine;
+                pend_nb = it.nb;
+            }
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+        if (pend_ti >= 0) {
+            bulk_wait0();
+            fence_proxy_async();
+            finish_tile(c, f.n2, pend_ti, pend_nb);
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+}
+
+cudaError_t configure_moe2() {
+    return cudaFuncSetAttribute(k_moe2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
+}
+
+cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
+                        const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st) {
+    Args f;
+    f.n1 = c.I / 128;
+    f.n2 = c.H / 256;
+    f.kb1 = c.H / kBK;
+    f.kb2 = c.I / kBK;
+    f.lag = std::max(1, (grid + f.n1 - 1) / f.n1);  // pairs: half as many concurrent items
+    f.pad = 0;
+    f.a1_row_base = a1_row_base;
+    DevCtx cc = c;
+    void* args[] = {const_cast<CUtensorMap*>(&a1), const_cast<CUtensorMap*>(&b1), const_cast<CUtensorMap*>(&a2),
+                    const_cast<CUtensorMap*>(&b2), &cc, &f};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid & ~1);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        cfg.numAttrs = 0;  // cooperative + clusters rejected: 1 CTA/SM, grid = #SMs keeps them co-resident
+        e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
+    }
+    return e;
+}
+
+}  // namespace perseus

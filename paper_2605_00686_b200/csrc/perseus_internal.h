@@ -82,6 +82,8 @@ struct PlanHeader {
     int32_t n_cgroups;
     int32_t total_tiles;    // reference tile ids in use (all PEs)
     int32_t error;
+    int32_t n_pairs;        // M-tile pairs (same expert) for the CTA-pair kernel
+    int32_t pad;
     int64_t remote_rows_in; // rows received from peers (heap rows before the self segment)
 };
 

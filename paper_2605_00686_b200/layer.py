@@ -41,7 +41,7 @@ class MoELayer:
     def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
                  device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
                  protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True,
-                 fused: bool = True):
+                 fused: bool = True, pair: bool = True):
         protocol = protocol or combined_protocol(0)
         self.fused = fused
         self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
@@ -50,7 +50,7 @@ class MoELayer:
                                tokens_per_pe, ROUTING[routing], float(skew), seed,
                                protocol.device_signaling(), protocol.group_size,
                                (_lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
-                               | (0 if fused else _lib.F_UNFUSED))
+                               | (0 if fused else _lib.F_UNFUSED) | (0 if pair else _lib.F_NO_PAIR))
         self._cfg = cfg
         h = C.c_void_p()
         check(lib.perseus_layer_create(C.byref(cfg), rank, world, device, C.byref(h)))

@@ -158,8 +158,9 @@ def test_qwen3_single_gpu_subset(oracle):
     _check_rank(oracle, pb, shape_of(m, S, 1), layers[0], xs[0], outs[0], "balanced", 1, 0.0, 0, subset=subset)
 
 
-@pytest.mark.parametrize("routing", ["balanced", "zipf", "gate"])
-def test_fused_kernel_bit_identical_to_stage_kernels(oracle, routing):
+@pytest.mark.parametrize("routing,pair", [("balanced", True), ("zipf", True), ("gate", True),
+                                          ("balanced", False), ("zipf", False)])
+def test_fused_kernel_bit_identical_to_stage_kernels(oracle, routing, pair):
     """The fused persistent kernel (dispatch + GEMM1 + GEMM2/combine-put, dynamic
     tile scheduler) computes exactly what the stage kernels compute."""
     import torch
@@ -169,7 +170,7 @@ def test_fused_kernel_bit_identical_to_stage_kernels(oracle, routing):
     S = 1024
     outs, cnts = [], []
     for fused in (True, False):
-        l = pb.MoELayer(m, S, routing=routing, skew=1.1, seed=9, fused=fused)
+        l = pb.MoELayer(m, S, routing=routing, skew=1.1, seed=9, fused=fused, pair=pair)
         x = torch.empty(S, m.hidden_dim, dtype=torch.bfloat16, device="cuda")
         l.fill_synthetic_x(x, 9)
         o = torch.empty_like(x)
