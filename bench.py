@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--config", default="qwen3", choices=list(CONFIGS))
     ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU (S)")
     ap.add_argument("--signaling", default="combined", choices=["combined", "vanilla", "decoupled"])
+    ap.add_argument("--group-size", type=int, default=0, help="decoupled signal group size (0 = per destination PE)")
     ap.add_argument("--routing", default="balanced", choices=["balanced", "zipf", "gate"])
     ap.add_argument("--skew", type=float, default=0.0)
     ap.add_argument("--ref-tokens", type=int, default=1024)
@@ -234,8 +235,8 @@ def main():
     cfg = CONFIGS[args.config]
     H, I, E, k, S = cfg["H"], cfg["I"], cfg["E"], cfg["k"], args.tokens
     model = pb.ModelConfig(args.config, H, I, E, k)
-    proto = {"combined": pb.combined_protocol(0), "vanilla": pb.vanilla_protocol(),
-             "decoupled": pb.decoupled_protocol(0)}[args.signaling]
+    proto = {"combined": pb.combined_protocol(args.group_size), "vanilla": pb.vanilla_protocol(),
+             "decoupled": pb.decoupled_protocol(args.group_size)}[args.signaling]
     layer = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing,
                         skew=args.skew, seed=1, protocol=proto, fused=not args.unfused,
                         pair=not args.no_pair)
@@ -339,6 +340,12 @@ def main():
         cpu = {"value": v, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind, "sample": desc}
 
     dc = {key: (c1[key] - c0[key]) / args.steps for key in c1 if key != "epoch"}
+    if dc.get("cta_ns"):
+        # fraction of the fused kernel's CTA time the producer waited on dependencies,
+        # and copy-warp busy fraction (per CTA: 2 copy warps)
+        dc["frac_wait_dispatch"] = dc["wait_dispatch_ns"] / dc["cta_ns"]
+        dc["frac_wait_g1"] = dc["wait_g1_ns"] / dc["cta_ns"]
+        dc["frac_copy_busy"] = dc["copy_ns"] / (6 * dc["cta_ns"])
     launches_per_step = 10
     if rank == 0:
         line = {
@@ -360,6 +367,7 @@ def main():
                                  st_mean)),
             "fused": not args.unfused,
             "cta_pairs": not args.no_pair and not args.unfused,
+            "group_size": args.group_size,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes},
             "roofline": roof,

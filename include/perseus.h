@@ -190,6 +190,10 @@ typedef struct perseus_counters {
     int64_t recv_tiles;            /* M-tiles processed by the expert FFN here */
     int64_t wait_timeouts;         /* bounded spin-waits that gave up (must be 0) */
     int64_t errors;                /* device-detected plan errors (must be 0) */
+    int64_t wait_dispatch_ns;      /* fused kernel, summed over CTAs: producer blocked on dispatch flags */
+    int64_t wait_g1_ns;            /* ... producer blocked on GEMM1->GEMM2 tile dependencies */
+    int64_t copy_ns;               /* ... copy warps busy with dispatch puts */
+    int64_t cta_ns;                /* ... CTA lifetimes (normaliser) */
 } perseus_counters;
 int perseus_layer_counters(perseus_layer* layer, perseus_counters* out);
 

@@ -49,7 +49,7 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "epoch", "dispatch_fences", "dispatch_signals", "dispatch_puts", "dispatch_put_bytes",
         "combine_fences", "combine_signals", "combine_puts", "combine_put_bytes", "recv_tiles",
-        "wait_timeouts", "errors")]
+        "wait_timeouts", "errors", "wait_dispatch_ns", "wait_g1_ns", "copy_ns", "cta_ns")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

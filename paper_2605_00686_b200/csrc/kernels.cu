@@ -415,23 +415,21 @@ __global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
             st.group = d == r ? -1 : (gs > 0 ? p / gs : dst_group[d]);
             st.recv_pos = -1;
             st.pad = 0;
-            // copy order: tile idx-major over destinations [self, remote ascending],
-            // so every receiver sees its sources' tiles arrive interleaved
-            const int idx = ch + (pos0 - dst_first[d]);
-            int so = 0;
-            for (int q = 0; q < P; ++q) {
-                const int dq = q == 0 ? r : (q <= r ? q - 1 : q);
-                so += min(dst_n[dq], idx) + ((dq == d) ? 0 : 0);
-            }
-            for (int q = 0; q < P; ++q) {
-                const int dq = q == 0 ? r : (q <= r ? q - 1 : q);
-                if (dq == d) break;
-                so += dst_n[dq] > idx;
+            // remote copy order: tile idx-major over the remote destinations, so
+            // every receiver sees its sources' tiles arrive interleaved in the
+            // order it consumes them (self tiles have their own queue)
+            if (d != r) {
+                const int idx = ch + (pos0 - dst_first[d]);
+                int so = 0;
+                for (int dq = 0; dq < P; ++dq) {
+                    if (dq == r) continue;
+                    so += min(dst_n[dq], idx) + ((dq < d && dst_n[dq] > idx) ? 1 : 0);
+                }
+                if (so < c.max_send) c.sorder[so] = p;
             }
             if (p < c.max_send) {
                 c.send[p] = st;
                 c.send_done[p] = 0;
-                c.sorder[so] = p;
             } else {
                 s_err = 3;
             }

@@ -512,6 +512,10 @@ int perseus_layer_counters(perseus_layer* L, perseus_counters* out) {
         out->recv_tiles = int64_t(s[kStatRecvTiles]);
         out->wait_timeouts = int64_t(s[kStatTimeouts]);
         out->errors = int64_t(s[kStatErrors]);
+        out->wait_dispatch_ns = int64_t(s[kStatWaitDispatchNs]);
+        out->wait_g1_ns = int64_t(s[kStatWaitG1Ns]);
+        out->copy_ns = int64_t(s[kStatCopyNs]);
+        out->cta_ns = int64_t(s[kStatCtaNs]);
     });
 }
 

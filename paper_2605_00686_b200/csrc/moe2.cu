@@ -42,7 +42,7 @@ constexpr int kTmemCols = 512;
 constexpr int kStgRow = 128 + 16;
 constexpr int kStgBytes = 128 * kStgRow;
 constexpr int kRing = 8;
-constexpr int kUnitRows = 16;
+constexpr int kUnitRows = 2;  // fine units: few tiles in flight, so tiles land one after another at link rate
 constexpr int kUnitsPerTile = kTileRows / kUnitRows;
 constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 
@@ -120,7 +120,7 @@ __device__ __forceinline__ uint32_t pk(const uint32_t* v, int i) {
 
 }  // namespace
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     k_moe2(const __grid_constant__ CUtensorMap tm_a1, const __grid_constant__ CUtensorMap tm_b1,
            const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b2, DevCtx c,
            Args f) {
@@ -171,10 +171,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    const uint64_t t_cta0 = globaltimer();
 
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- scheduler (leader) + TMA producer (both) ----------------
+            unsigned long long wait_d = 0, wait_g = 0;
             int stage = 0, slot = 0;
             uint32_t phase = 0, rphase = 0;
             const uint32_t* dflags = c.dflag[c.rank] + size_t(c.par) * c.T_max;
@@ -202,10 +204,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 int32_t a_row, b_row, nkb;
                 const CUtensorMap* ta;
                 const CUtensorMap* tb;
+                const uint64_t tw0 = globaltimer();
                 if (it.kind == 1) {
                     const bool ok = rt.tile_id >= 0 ? wait_flag_geq(dflags + rt.tile_id, c.epoch, kWaitTimeoutNs)
                                                     : wait_flag_geq(c.self_ready + mine, c.epoch, kWaitTimeoutNs);
                     if (!ok) atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                    wait_d += globaltimer() - tw0;
                     a_row = int32_t(f.a1_row_base + rt.heap_row);
                     b_row = rt.e_local * 2 * c.I + it.nb * 128 + (crank ? c.I : 0);  // gate | up
                     nkb = f.kb1;
@@ -214,6 +218,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 } else {
                     if (!wait_flag_geq(c.g1_done + mine, uint32_t(f.n1), kWaitTimeoutNs))
                         atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                    wait_g += globaltimer() - tw0;
                     a_row = int32_t(rt.heap_row);
                     b_row = rt.e_local * c.H + it.nb * 256 + int(crank) * 128;
                     nkb = f.kb2;
@@ -231,6 +236,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
+            atomicAdd(&c.stats[kStatWaitDispatchNs], wait_d);
+            atomicAdd(&c.stats[kStatWaitG1Ns], wait_g);
         }
     } else if (warp == 1) {
         if (lane == 0 && lead) {
@@ -265,15 +272,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
         }
-    } else if (warp < 4) {
+    } else if (warp < 4 || warp >= 8) {
         // ---------------- copy warps: dispatch puts ----------------
-        const int total_units = hdr.n_send * kUnitsPerTile;
+        // Two queues started at t=0: self tiles (local copy; the GEMM consumes
+        // them first) and remote tiles (NVLink, dst-interleaved).  Warps 2-3
+        // drain the self queue first, warps 8-11 the remote queue first.
+        const int remote_units = hdr.n_send_remote * kUnitsPerTile;
+        const int self_units = (hdr.n_send - hdr.n_send_remote) * kUnitsPerTile;
+        const uint64_t tc0 = globaltimer();
+        bool remote_q = warp >= 8;
+        bool other_done = false;
         while (true) {
             int u = 0;
-            if (lane == 0) u = int(atomicAdd(&c.sched[1], 1u));
+            if (lane == 0) u = int(atomicAdd(&c.sched[remote_q ? 1 : 2], 1u));
             u = __shfl_sync(0xffffffffu, u, 0);
-            if (u >= total_units) break;
-            const int sp = c.sorder[u / kUnitsPerTile];
+            if (u >= (remote_q ? remote_units : self_units)) {
+                if (other_done) break;
+                other_done = true;
+                remote_q = !remote_q;
+                continue;
+            }
+            const int sp = remote_q ? c.sorder[u / kUnitsPerTile] : hdr.n_send_remote + u / kUnitsPerTile;
             const SendTile st = c.send[sp];
             const int r0 = (u % kUnitsPerTile) * kUnitRows;
             if (r0 >= st.rows) continue;
@@ -299,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
                                 kStatDispatchFences, kStatDispatchSignals);
         }
+        if (lane == 0) atomicAdd(&c.stats[kStatCopyNs], (unsigned long long)(globaltimer() - tc0));
     } else {
         // ---------------- epilogue (4 warps, this CTA's 128 accumulator rows) ----------------
         const int q = warp & 3;
@@ -423,6 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
+    if (threadIdx.x == 0) atomicAdd(&c.stats[kStatCtaNs], (unsigned long long)(globaltimer() - t_cta0));
     if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 
@@ -445,7 +466,7 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
                     const_cast<CUtensorMap*>(&b2), &cc, &f};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid & ~1);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(384);  // warps 2-3 and 8-11 copy, 4-7 epilogue
     cfg.dynamicSmemBytes = kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

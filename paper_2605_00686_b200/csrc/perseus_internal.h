@@ -100,6 +100,10 @@ enum StatSlot : int {
     kStatRecvTiles,
     kStatTimeouts,
     kStatErrors,
+    kStatWaitDispatchNs,  // fused kernel: producer time blocked on dispatch / self-ready flags
+    kStatWaitG1Ns,        // ... blocked on GEMM1 -> GEMM2 tile dependencies
+    kStatCopyNs,          // ... copy-warp busy time (dispatch puts)
+    kStatCtaNs,           // ... summed CTA lifetimes
     kStatCount
 };
 
