@@ -312,26 +312,53 @@ def main():
     e2e_value = world * S * args.steps / float(te.item())
     clk.__exit__(None, None, None)
 
-    # ---- roofline of the dominant kernel (GEMM1 + SwiGLU, tcgen05) ----
+    # ---- roofline of the dominant kernel ----
+    # fused path: k_moe2 / k_moe (dispatch puts + GEMM1/SwiGLU + GEMM2/combine puts);
+    # unfused path: k_gemm<1> (GEMM1 + SwiGLU).  Algorithmic work per launch on
+    # this GPU (balanced routing: S*k rows received per PE):
+    #   FLOP  = 6*H*I*rows (4HI gate+up, 2HI down)
+    #   bytes = expert weights (E/P)*3*H*I*2 + heap round trip 2*rows*H*2 (dispatch
+    #           write, GEMM1 read) + h round trip 2*rows*I*2 + y write rows*H*2
     peaks, peaks_src = measured_peaks()
-    rows = S * k  # rows through the expert FFN on this GPU (balanced: S*k per PE)
-    flops_g1 = 2.0 * rows * H * (2 * I)
-    flops_g2 = 2.0 * rows * I * H
-    g1_ms = st_mean[2]
-    g2_ms = st_mean[3]
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    ach = flops_g1 / (g1_ms / 1e3) / 1e12
-    roof = {"kernel": "k_gemm<1> (GEMM1 + fused SwiGLU, tcgen05)", "bound": "tensor", "achieved": ach,
-            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-            "peak_source": f"{peaks_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
-            "algorithmic": f"2*{rows}*{H}*{2 * I} FLOP per launch",
-            "gemm2": {"achieved": flops_g2 / (g2_ms / 1e3) / 1e12, "frac": flops_g2 / (g2_ms / 1e3) / 1e12 / peak},
-            "ffn": {"achieved": (flops_g1 + flops_g2) / ((g1_ms + g2_ms) / 1e3) / 1e12,
-                    "frac": (flops_g1 + flops_g2) / ((g1_ms + g2_ms) / 1e3) / 1e12 / peak}}
-    # layer roofline: slower of compute-at-peak and bytes-over-NVLink (770 GB/s per direction)
+    rows = S * k
+    tflops_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    if not args.unfused:
+        kname = "k_moe2 (fused dispatch + GEMM1/SwiGLU + GEMM2/combine-put, tcgen05 cta_group::2)" if not args.no_pair \
+            else "k_moe (fused, tcgen05 cta_group::1)"
+        k_ms = st_mean[2]
+        k_flop = 6.0 * H * I * rows
+        k_bytes = (E // world) * 3.0 * H * I * 2 + 2.0 * rows * H * 2 + 2.0 * rows * I * 2 + rows * H * 2.0
+    else:
+        kname = "k_gemm<1> (GEMM1 + fused SwiGLU, tcgen05)"
+        k_ms = st_mean[2]
+        k_flop = 4.0 * H * I * rows
+        k_bytes = (E // world) * 2.0 * H * I * 2 + rows * H * 2.0 + rows * I * 2.0
+    t_tensor = k_flop / (tflops_peak * 1e12)
+    t_hbm = k_bytes / (hbm_peak * 1e9)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(f"{args.config}_ep{world}_{'fused' if not args.unfused else 'unfused'}")
+    ach_tf = k_flop / (k_ms / 1e3) / 1e12
+    ach_gb = k_bytes / (k_ms / 1e3) / 1e9
+    if t_hbm >= t_tensor:
+        roof = {"kernel": kname, "bound": "hbm", "achieved": ach_gb, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach_gb / hbm_peak, "traffic": traffic}
+    else:
+        roof = {"kernel": kname, "bound": "tensor", "achieved": ach_tf, "peak": tflops_peak, "unit": "TFLOP/s",
+                "frac": ach_tf / tflops_peak, "traffic": traffic}
+    roof.update({"peak_source": f"{peaks_src} MEASURED_PEAKS.json (hbm_gbs / bf16_tflops_sustained)",
+                 "launch_ms": k_ms, "algorithmic_flop": k_flop, "algorithmic_bytes": k_bytes,
+                 "tensor": {"achieved_tflops": ach_tf, "frac": ach_tf / tflops_peak},
+                 "hbm": {"achieved_gbs": ach_gb, "frac": ach_gb / hbm_peak},
+                 "timing": "CUDA events on the layer stream around the kernel, mean of 10 synchronised steps"})
+    # layer roofline: slowest of tensor-at-peak, HBM bytes and bytes-over-NVLink (770 GB/s/direction measured)
     flops_layer = 6.0 * H * I * S * k + 2.0 * S * H * E
     nvl_bytes = 2.0 * S * k * (world - 1) / world * H * 2
-    t_roof = max(flops_layer / (peak * 1e12), nvl_bytes / 770e9)
+    hbm_layer = (E // world) * 3.0 * H * I * 2 + 2.0 * rows * H * 2 + 2.0 * rows * I * 2 + 2.0 * rows * H * 2
+    t_roof = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / 770e9, hbm_layer / (hbm_peak * 1e9))
     layer_frac = t_roof / (ms_step / 1e3)
 
     cpu = None
@@ -345,7 +372,7 @@ def main():
         # and copy-warp busy fraction (per CTA: 2 copy warps)
         dc["frac_wait_dispatch"] = dc["wait_dispatch_ns"] / dc["cta_ns"]
         dc["frac_wait_g1"] = dc["wait_g1_ns"] / dc["cta_ns"]
-        dc["frac_copy_busy"] = dc["copy_ns"] / (6 * dc["cta_ns"])
+        dc["frac_copy_busy"] = dc["copy_ns"] / ((6 if not args.no_pair else 2) * dc["cta_ns"])
     launches_per_step = 10
     if rank == 0:
         line = {
@@ -369,7 +396,10 @@ def main():
             "cta_pairs": not args.no_pair and not args.unfused,
             "group_size": args.group_size,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
-                               "flops": flops_layer, "nvlink_bytes": nvl_bytes},
+                               "flops": flops_layer, "nvlink_bytes": nvl_bytes, "hbm_bytes": hbm_layer,
+                               "t_tensor_us": flops_layer / (tflops_peak * 1e12) * 1e6,
+                               "t_nvlink_us": nvl_bytes / 770e9 * 1e6,
+                               "t_hbm_us": hbm_layer / (hbm_peak * 1e9) * 1e6},
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": S * H * 2,
                     "d2h_bytes_per_step": S * H * 2,

@@ -1,10 +1,11 @@
 set -x
+nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; tail -c 4000 gpurun_out/bench_full.log
 B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
-timeout 300 $B > gpurun_out/plain.log 2>&1; tail -c 600 gpurun_out/plain.log
-timeout 300 $B --unfused > gpurun_out/plain_unfused.log 2>&1; tail -c 600 gpurun_out/plain_unfused.log
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none \
-  -k regex:"k_(gate|route|hist|perm|publish|plan|dispatch|gemm|combine|moe)" -s 24 -c 24 \
-  --csv --log-file gpurun_out/launches_fused.csv $B > gpurun_out/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_moe" -s 3 -c 1 \
-  -o gpurun_out/prof_moe $B > gpurun_out/ncu_full.log 2>&1
+timeout 300 $B > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k regex:"k_(gate|route|perm|plan|gemm|combine|moe)" -s 18 -c 18 \
+  --csv --log-file gpurun_out/launches_r01.csv $B > gpurun_out/ncu_launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_moe2" -s 3 -c 1 \
+  -o gpurun_out/prof_moe2 $B > gpurun_out/ncu_full.log 2>&1
 tail -2 gpurun_out/ncu_full.log
