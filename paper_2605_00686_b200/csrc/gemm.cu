@@ -398,7 +398,7 @@ __device__ __forceinline__ Item item_of(int w, int T, const FusedArgs& f) {
 }
 
 constexpr int kRing = 8;
-constexpr int kUnitRows = 16;
+constexpr int kUnitRows = 2;
 constexpr int kUnitsPerTile = kTileRows / kUnitRows;
 
 __device__ __forceinline__ void copy_unit_warp(const DevCtx& c, const SendTile& st, int r0, int nrows, int lane) {
@@ -557,13 +557,21 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp < 4) {
         // ---------------- copy warps: dispatch puts ----------------
-        const int total_units = hdr.n_send * kUnitsPerTile;
+        // self queue (warp 2 first) and remote queue (warp 3 first), as in k_moe2
+        const int remote_units = hdr.n_send_remote * kUnitsPerTile;
+        const int self_units = (hdr.n_send - hdr.n_send_remote) * kUnitsPerTile;
+        bool remote_q = warp == 3, other_done = false;
         while (true) {
             int u = 0;
-            if (lane == 0) u = int(atomicAdd(&c.sched[1], 1u));
+            if (lane == 0) u = int(atomicAdd(&c.sched[remote_q ? 1 : 2], 1u));
             u = __shfl_sync(0xffffffffu, u, 0);
-            if (u >= total_units) break;
-            const int sp = c.sorder[u / kUnitsPerTile];
+            if (u >= (remote_q ? remote_units : self_units)) {
+                if (other_done) break;
+                other_done = true;
+                remote_q = !remote_q;
+                continue;
+            }
+            const int sp = remote_q ? c.sorder[u / kUnitsPerTile] : hdr.n_send_remote + u / kUnitsPerTile;
             const SendTile st = c.send[sp];
             const int r0 = (u % kUnitsPerTile) * kUnitRows;
             if (r0 >= st.rows) continue;

@@ -303,315 +303,7 @@ __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33
 
 __device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 
-// The per-forward layout, computed on the device from the [P][E] count table
-// every rank published.  It reproduces the reference's layout exactly:
-//   tile ids     — global counter in (src, expert, chunk) order over remote
-//                  pairs (workload.cpp:136-149, with tile_bytes = 128*H*2)
-//   heap offsets — per-destination cursor in the same order (:146-147)
-//   groups       — (dst, expert, tile) order; per-dst or fixed size
-//                  (protocols.cpp:52-94)
-__global__ void __launch_bounds__(1024) k_plan(DevCtx c) {
-    extern __shared__ int32_t sm[];
-    const int P = c.P, E = c.E, El = c.E_loc, r = c.rank, tid = threadIdx.x;
-    const int PE = P * E;
-    int32_t* T = sm;              // [P][E] counts
-    int32_t* tb = T + PE;         // tile-id base per (s, e), s-major
-    int32_t* hr = tb + PE;        // heap row scan, (d, s, j) order
-    int32_t* off = hr + PE;       // sorted offsets per (s, e)
-    int32_t* sp = off + PE;       // send position per e (key order)
-    int32_t* rp = sp + E;         // recv position per (ks, j)
-    int32_t* scratch = rp + E;    // 33 (+pad)
-    int32_t* selfo = scratch + 40;  // [El] self-segment row offsets
-    int32_t* tb2 = selfo + El;      // [P*E] scratch
-    int32_t* ppos = tb2 + PE;       // [E] pair position per (ks, j)
-    __shared__ int32_t src_pfirst[kMaxPes], src_np[kMaxPes];
-    __shared__ int32_t s_err;
-    __shared__ int32_t dst_first[kMaxPes + 1], dst_group[kMaxPes], src_first[kMaxPes + 1],
-        src_group[kMaxPes], dst_n[kMaxPes], src_n[kMaxPes];
-
-    if (tid == 0) s_err = 0;
-    if (tid < P) {
-        if (!wait_flag_geq(c.count_flag[r] + tid, c.epoch, kWaitTimeoutNs)) {
-            atomicAdd(&c.stats[kStatTimeouts], 1ull);
-            s_err = 1;
-        }
-    }
-    __syncthreads();
-    const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
-    for (int i = tid; i < PE; i += 1024) {
-        const int32_t v = ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i));
-        const int s = i / E, e = i % E;
-        T[i] = v;
-        tb[i] = (s != e % P) ? ceil_tiles(v) : 0;
-        off[i] = v;
-        const int d = e % P, j = e / P;
-        hr[(d * P + s) * El + j] = (s != d) ? v : 0;
-    }
-    __syncthreads();
-    const int32_t total_tiles = block_exclusive_scan(tb, PE, scratch);
-    const int32_t total_hr = block_exclusive_scan(hr, PE, scratch);
-    // rows received here from peers: the extent of destination block r
-    const int32_t rows_in_r = (r + 1 < P ? hr[(r + 1) * P * El] : total_hr) - hr[r * P * El];
-    // sorted offsets inside each source: one scan over [P][E], minus row starts
-    block_exclusive_scan(off, PE, scratch);
-    for (int i = tid; i < PE; i += 1024) tb2[i] = off[(i / E) * E];  // row start
-    // self-segment offsets of this rank's local experts (e = r + P*j)
-    for (int j = tid; j < El; j += 1024) selfo[j] = T[r * E + r + P * j];
-    __syncthreads();
-    for (int i = tid; i < PE; i += 1024) off[i] -= tb2[i];
-    block_exclusive_scan(selfo, El, scratch);
-
-    // ---- send side (this rank as source) ----
-    // key order: remote destinations ascending, then the self segment
-    for (int e = tid; e < E; e += 1024) {
-        const int d = e % P, j = e / P;
-        const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
-        sp[kd * El + j] = ceil_tiles(T[r * E + e]);
-    }
-    __syncthreads();
-    const int32_t n_send = block_exclusive_scan(sp, E, scratch);
-    if (tid == 0) {
-        // first send position of every destination + dense per-dst group ids
-        int g = 0;
-        for (int kd = 0; kd < P; ++kd) {
-            const int d = kd < r ? kd : (kd < P - 1 ? kd + 1 : r);
-            const int first = sp[kd * El];
-            const int last = kd + 1 < P ? sp[(kd + 1) * El] : n_send;
-            dst_first[d] = first;
-            dst_n[d] = last - first;
-            dst_group[d] = (d != r && last > first) ? g++ : -1;
-        }
-        dst_first[kMaxPes] = g;
-        for (int q = 0; q < 4; ++q) c.sched[q] = 0;
-    }
-    __syncthreads();
-    const int32_t n_send_remote = dst_first[r];
-    const int gs = c.group_size;
-    if (gs > 0 && n_send_remote % gs != 0) s_err = 2;
-    const int32_t n_groups = gs > 0 ? n_send_remote / gs : dst_first[kMaxPes];
-
-    for (int e = tid; e < E; e += 1024) {
-        const int d = e % P, j = e / P;
-        const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
-        const int32_t cnt = T[r * E + e];
-        const int nt = ceil_tiles(cnt);
-        int32_t pos0 = sp[kd * El + j];
-        int64_t hrow;
-        if (d != r) {
-            hrow = hr[(d * P + r) * El + j] - hr[d * P * El];
-        } else {
-            hrow = rows_in_r + selfo[j];
-        }
-        c.send_first[e] = pos0;
-        for (int ch = 0; ch < nt; ++ch) {
-            SendTile st;
-            st.expert = e;
-            st.dst = d;
-            st.row0 = ch * kTileRows;
-            st.rows = min(kTileRows, cnt - ch * kTileRows);
-            st.heap_row = hrow + int64_t(ch) * kTileRows;
-            st.tile_id = d != r ? tb[r * E + e] + ch : -1;
-            const int p = pos0 + ch;
-            st.group = d == r ? -1 : (gs > 0 ? p / gs : dst_group[d]);
-            st.recv_pos = -1;
-            st.pad = 0;
-            // remote copy order: tile idx-major over the remote destinations, so
-            // every receiver sees its sources' tiles arrive interleaved in the
-            // order it consumes them (self tiles have their own queue)
-            if (d != r) {
-                const int idx = ch + (pos0 - dst_first[d]);
-                int so = 0;
-                for (int dq = 0; dq < P; ++dq) {
-                    if (dq == r) continue;
-                    so += min(dst_n[dq], idx) + ((dq < d && dst_n[dq] > idx) ? 1 : 0);
-                }
-                if (so < c.max_send) c.sorder[so] = p;
-            }
-            if (p < c.max_send) {
-                c.send[p] = st;
-                c.send_done[p] = 0;
-            } else {
-                s_err = 3;
-            }
-        }
-    }
-    // groups (dispatch direction)
-    if (gs > 0) {
-        for (int g = tid; g < n_groups; g += 1024) {
-            Group G;
-            G.first = g * gs;
-            G.count = gs;
-            G.peer = -1;
-            G.pad = 0;
-            c.groups[g] = G;
-            c.group_ctr[g] = 0;
-        }
-    } else if (tid < P && tid != r && dst_group[tid] >= 0) {
-        const int d = tid;
-        int kd = d < r ? d : d - 1;
-        const int last = kd + 1 < P ? sp[(kd + 1) * El] : n_send;
-        Group G;
-        G.peer = d;
-        G.first = dst_first[d];
-        G.count = last - dst_first[d];
-        G.pad = 0;
-        c.groups[dst_group[d]] = G;
-        c.group_ctr[dst_group[d]] = 0;
-    }
-
-    // ---- receive side (this rank as destination) ----
-    for (int i = tid; i < P * El; i += 1024) {
-        const int s = i / El, j = i % El;
-        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
-        rp[ks * El + j] = ceil_tiles(T[s * E + r + P * j]);
-    }
-    __syncthreads();
-    const int32_t n_recv = block_exclusive_scan(rp, P * El, scratch);
-    if (tid == 0) {
-        int g = 0;
-        for (int ks = 0; ks < P; ++ks) {
-            const int s = ks == 0 ? r : (ks <= r ? ks - 1 : ks);
-            const int first = rp[ks * El];
-            const int last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
-            src_first[s] = first;
-            src_n[s] = last - first;
-            src_group[s] = (s != r && last > first) ? g++ : -1;
-        }
-    }
-    __syncthreads();
-    const int32_t n_recv_self = (P > 1) ? rp[El] : n_recv;
-    const int32_t n_recv_remote = n_recv - n_recv_self;
-    if (gs > 0 && n_recv_remote % gs != 0) s_err = 4;
-    int32_t n_cgroups = 0;
-    if (gs > 0) n_cgroups = n_recv_remote / gs;
-    else for (int s = 0; s < P; ++s) n_cgroups += src_group[s] >= 0;
-
-    for (int i = tid; i < P * El; i += 1024) {
-        const int s = i / El, j = i % El, e = r + P * j;
-        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
-        const int32_t cnt = T[s * E + e];
-        const int nt = ceil_tiles(cnt);
-        const int32_t pos0 = rp[ks * El + j];
-        int64_t hrow;
-        if (s != r) {
-            hrow = hr[(r * P + s) * El + j] - hr[r * P * El];
-        } else {
-            hrow = rows_in_r + selfo[j];
-        }
-        for (int ch = 0; ch < nt; ++ch) {
-            RecvTile rt;
-            rt.src = s;
-            rt.e_local = j;
-            rt.rows = min(kTileRows, cnt - ch * kTileRows);
-            rt.tile_id = s != r ? tb[s * E + e] + ch : -1;
-            rt.heap_row = hrow + int64_t(ch) * kTileRows;
-            rt.ybuf_row = off[s * E + e] + int64_t(ch) * kTileRows;
-            const int p = pos0 + ch;
-            rt.cgroup = s == r ? -1 : (gs > 0 ? (p - n_recv_self) / gs : src_group[s]);
-            rt.pad = 0;
-            // processing order: self tiles first, then remote tiles idx-major
-            // over sources (the order the interleaved copies arrive in)
-            int ro = p;
-            if (s != r) {
-                const int idx = p - src_first[s];
-                ro = n_recv_self;
-                for (int q = 0; q < P; ++q)
-                    if (q != r) ro += min(src_n[q], idx) + ((q < s && src_n[q] > idx) ? 1 : 0);
-            } else {
-                // link the matching self send tile (self is last in send key order)
-                const int sp_self = sp[(P - 1) * El + j] + ch;
-                if (sp_self < c.max_send) c.send[sp_self].recv_pos = p;
-            }
-            if (p < c.max_recv && ro < c.max_recv) {
-                c.recv[p] = rt;
-                c.tile_ctr[p] = 0;
-                c.g1_done[p] = 0;
-                c.rorder[ro] = p;
-            } else {
-                s_err = 5;
-            }
-        }
-    }
-    if (gs > 0) {
-        for (int g = tid; g < n_cgroups; g += 1024) {
-            Group G;
-            G.first = n_recv_self + g * gs;
-            G.count = gs;
-            G.peer = -1;
-            G.pad = 0;
-            c.cgroups[g] = G;
-            c.cgroup_ctr[g] = 0;
-        }
-    } else if (tid < P && tid != r && src_group[tid] >= 0) {
-        const int s = tid;
-        const int ks = s < r ? s + 1 : s;
-        const int last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
-        Group G;
-        G.peer = s;
-        G.first = src_first[s];
-        G.count = last - src_first[s];
-        G.pad = 0;
-        c.cgroups[src_group[s]] = G;
-        c.cgroup_ctr[src_group[s]] = 0;
-    }
-    // ---- M-tile pairs for the CTA-pair (cta_group::2) kernel: consecutive
-    // chunks of one (src, expert) segment share the expert's weights; an odd
-    // last chunk is paired with nothing (-1).  Pair order mirrors rorder.
-    for (int i = tid; i < P * El; i += 1024) {
-        const int s = i / El, j = i % El;
-        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
-        ppos[ks * El + j] = (ceil_tiles(T[s * E + r + P * j]) + 1) / 2;
-    }
-    __syncthreads();
-    const int32_t n_pairs = block_exclusive_scan(ppos, P * El, scratch);
-    if (tid == 0) {
-        for (int ks = 0; ks < P; ++ks) {
-            const int s = ks == 0 ? r : (ks <= r ? ks - 1 : ks);
-            const int first = ppos[ks * El];
-            src_pfirst[s] = first;
-            src_np[s] = (ks + 1 < P ? ppos[(ks + 1) * El] : n_pairs) - first;
-        }
-    }
-    __syncthreads();
-    const int32_t n_pairs_self = src_np[r];
-    for (int i = tid; i < P * El; i += 1024) {
-        const int s = i / El, j = i % El;
-        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
-        const int nt = ceil_tiles(T[s * E + r + P * j]);
-        const int32_t pos0 = rp[ks * El + j];
-        for (int pi = 0; 2 * pi < nt; ++pi) {
-            const int q = ppos[ks * El + j] + pi;
-            int po = q;
-            if (s != r) {
-                const int idx = q - src_pfirst[s];
-                po = n_pairs_self;
-                for (int z = 0; z < P; ++z)
-                    if (z != r) po += min(src_np[z], idx) + ((z < s && src_np[z] > idx) ? 1 : 0);
-            }
-            if (po < c.max_recv) {
-                c.pairs[2 * po] = pos0 + 2 * pi;
-                c.pairs[2 * po + 1] = 2 * pi + 1 < nt ? pos0 + 2 * pi + 1 : -1;
-            }
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        PlanHeader h;
-        h.n_send = n_send;
-        h.n_send_remote = n_send_remote;
-        h.n_groups = n_groups;
-        h.n_recv = n_recv;
-        h.n_recv_remote = n_recv_remote;
-        h.n_cgroups = n_cgroups;
-        h.total_tiles = total_tiles;
-        h.error = s_err;
-        h.n_pairs = n_pairs;
-        h.pad = 0;
-        h.remote_rows_in = rows_in_r;
-        *c.hdr = h;
-        if (s_err) atomicAdd(&c.stats[kStatErrors], 1ull);
-    }
-}
+// (The per-forward plan is in plan.cu.)
 
 // -------------------------------------------------------------- dispatch ----
 // One CTA per send tile: gather the tile's token rows (sorted order) and store
@@ -725,12 +417,10 @@ size_t perm_smem_bytes(const DevCtx& c) {
     return sizeof(int32_t) * (size_t(c.E) * (kPermT / 32) + 2 * size_t(c.E) + 40);
 }
 
-size_t plan_smem_bytes(const DevCtx& c) {
-    const size_t PE = size_t(c.P) * c.E;
-    return sizeof(int32_t) * (5 * PE + 4 * size_t(c.E) + 48);
-}
 
-void launch_plan(const DevCtx& c, cudaStream_t st) { k_plan<<<1, 1024, plan_smem_bytes(c), st>>>(c); }
+void launch_plan4(const DevCtx& c, cudaStream_t st);
+cudaError_t configure_plan4(const DevCtx& c);
+void launch_plan(const DevCtx& c, cudaStream_t st) { launch_plan4(c, st); }
 
 void launch_dispatch(const DevCtx& c, cudaStream_t st) {
     launch_plan(c, st);
@@ -749,8 +439,7 @@ void launch_combine(const DevCtx& c, cudaStream_t st) {
 }
 
 cudaError_t configure_kernels(const DevCtx& c) {
-    cudaError_t e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(plan_smem_bytes(c)));
+    cudaError_t e = configure_plan4(c);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(perm_smem_bytes(c)));
 }

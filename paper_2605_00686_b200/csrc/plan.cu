@@ -1,0 +1,297 @@
+// plan.cu — the per-forward device plan, 4 warps, warp-level scans.
+//
+// Computes, from the [P][E] per-(src, expert) count table every rank
+// published, exactly the reference's dispatch layout (workload.cpp:132-213):
+//   tile ids     — global counter in (src, expert, chunk) order over remote
+//                  pairs (tile_bytes = 128*H*2, workload.cpp:136-149)
+//   heap offsets — per-destination cursor in the same order (:146-147)
+//   groups       — (dst, expert, tile) order; per destination or fixed size
+//                  (assign_groups, protocols.cpp:52-94)
+// plus the device-only schedules of the fused kernels (copy order, processing
+// order, M-tile pairs).  The plan is latency-bound (a few thousand integers),
+// so it runs as 4 independent warps with shuffle scans and three CTA
+// barriers, instead of block-wide scans over 1024 threads.
+#include <cuda_runtime.h>
+
+#include "layer_dev.h"
+#include "perseus.h"
+#include "ptx.cuh"
+
+namespace perseus {
+
+using namespace ptx;
+
+namespace {
+
+__device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
+
+// exclusive scan of a[0..n) in place by ONE warp; returns the total
+__device__ int32_t warp_scan(int32_t* a, int n) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    const int per = (n + 31) / 32, b = lane * per, e = min(n, b + per);
+    int32_t local = 0;
+    for (int i = b; i < e; ++i) local += a[i];
+    int32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    int32_t run = incl - local;
+    for (int i = b; i < e; ++i) {
+        const int32_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    return total;
+}
+
+// position of item `idx` of stream q in an idx-major interleave of streams
+// with lengths n[0..P) (streams listed in `order`, skipping `skip`)
+__device__ __forceinline__ int interleave_pos(const int32_t* n, int P, int skip, int q, int idx) {
+    int pos = 0;
+    for (int z = 0; z < P; ++z) {
+        if (z == skip) continue;
+        pos += min(n[z], idx) + ((z < q && n[z] > idx) ? 1 : 0);
+    }
+    return pos;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
+    extern __shared__ int32_t sm[];
+    const int P = c.P, E = c.E, El = c.E_loc, r = c.rank;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int PE = P * E;
+    int32_t* T = sm;            // [P][E] counts
+    int32_t* tb = T + PE;       // tile-id base per (s, e), s-major
+    int32_t* hr = tb + PE;      // heap-row scan, (d, s, j) order
+    int32_t* off = hr + PE;     // sorted offset per (s, e)
+    int32_t* sp = off + PE;     // send position per (kd, j)
+    int32_t* rp = sp + E;       // recv position per (ks, j)
+    int32_t* pp = rp + E;       // pair position per (ks, j)
+    int32_t* selfo = pp + E;    // [El] self-segment row offsets
+    __shared__ int32_t s_err, s_total_tiles, s_rows_in, s_n_send, s_n_recv, s_n_pairs;
+    __shared__ int32_t dst_first[kMaxPes], dst_n[kMaxPes], dst_group[kMaxPes], n_dgroups;
+    __shared__ int32_t src_first[kMaxPes], src_n[kMaxPes], src_group[kMaxPes], n_cgroups_pe;
+    __shared__ int32_t src_pfirst[kMaxPes], src_np[kMaxPes];
+
+    if (tid == 0) s_err = 0;
+    if (tid < P && !wait_flag_geq(c.count_flag[r] + tid, c.epoch, kWaitTimeoutNs)) {
+        atomicAdd(&c.stats[kStatTimeouts], 1ull);
+        s_err = 1;
+    }
+    __syncthreads();
+    const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
+    for (int i = tid; i < PE; i += 128) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
+    if (tid == 0) {
+        for (int q = 0; q < 4; ++q) c.sched[q] = 0;
+    }
+    __syncthreads();
+
+    // ---- phase B: four independent scans ----
+    if (warp == 0) {
+        for (int s = 0; s < P; ++s)
+            for (int e = lane; e < E; e += 32) tb[s * E + e] = (s != e % P) ? ceil_tiles(T[s * E + e]) : 0;
+        const int32_t tot = warp_scan(tb, PE);
+        if (lane == 0) s_total_tiles = tot;
+    } else if (warp == 1) {
+        // (d, s, j): the rows source s sends to destination d, in the reference's cursor order
+        for (int d = 0; d < P; ++d)
+            for (int s = 0; s < P; ++s)
+                for (int j = lane; j < El; j += 32) hr[(d * P + s) * El + j] = (s != d) ? T[s * E + d + P * j] : 0;
+        const int32_t tot = warp_scan(hr, PE);
+        if (lane == 0) s_rows_in = (r + 1 < P ? hr[(r + 1) * P * El] : tot) - hr[r * P * El];
+    } else if (warp == 2) {
+        for (int s = 0; s < P; ++s) {
+            for (int e = lane; e < E; e += 32) off[s * E + e] = T[s * E + e];
+            warp_scan(off + s * E, E);
+        }
+        for (int j = lane; j < El; j += 32) selfo[j] = T[r * E + r + P * j];
+        warp_scan(selfo, El);
+    } else {
+        // send key order: remote destinations ascending, then the self segment
+        for (int d = 0; d < P; ++d) {
+            const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
+            for (int j = lane; j < El; j += 32) sp[kd * El + j] = ceil_tiles(T[r * E + d + P * j]);
+        }
+        const int32_t n_send = warp_scan(sp, E);
+        // receive key order: self first, then remote sources ascending
+        for (int s = 0; s < P; ++s) {
+            const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+            for (int j = lane; j < El; j += 32) {
+                const int32_t nt = ceil_tiles(T[s * E + r + P * j]);
+                rp[ks * El + j] = nt;
+                pp[ks * El + j] = (nt + 1) / 2;
+            }
+        }
+        const int32_t n_recv = warp_scan(rp, E);
+        const int32_t n_pairs = warp_scan(pp, E);
+        if (lane == 0) {
+            s_n_send = n_send;
+            s_n_recv = n_recv;
+            s_n_pairs = n_pairs;
+            int g = 0;
+            for (int kd = 0; kd < P; ++kd) {
+                const int d = kd < r ? kd : (kd < P - 1 ? kd + 1 : r);
+                const int first = sp[kd * El];
+                const int last = kd + 1 < P ? sp[(kd + 1) * El] : n_send;
+                dst_first[d] = first;
+                dst_n[d] = last - first;
+                dst_group[d] = (d != r && last > first) ? g++ : -1;
+            }
+            n_dgroups = g;
+            g = 0;
+            for (int ks = 0; ks < P; ++ks) {
+                const int s = ks == 0 ? r : (ks <= r ? ks - 1 : ks);
+                const int first = rp[ks * El], last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
+                src_first[s] = first;
+                src_n[s] = last - first;
+                src_group[s] = (s != r && last > first) ? g++ : -1;
+                const int pf = pp[ks * El], pl = ks + 1 < P ? pp[(ks + 1) * El] : n_pairs;
+                src_pfirst[s] = pf;
+                src_np[s] = pl - pf;
+            }
+            n_cgroups_pe = g;
+        }
+    }
+    __syncthreads();
+
+    const int gs = c.group_size;
+    const int32_t n_send = s_n_send, n_recv = s_n_recv, n_pairs = s_n_pairs, rows_in_r = s_rows_in;
+    const int32_t n_send_remote = P > 1 ? dst_first[r] : 0;
+    const int32_t n_recv_self = src_n[r];
+    const int32_t n_recv_remote = n_recv - n_recv_self;
+    const int32_t n_groups = gs > 0 ? n_send_remote / gs : n_dgroups;
+    const int32_t n_cgroups = gs > 0 ? n_recv_remote / gs : n_cgroups_pe;
+    if (tid == 0 && gs > 0 && (n_send_remote % gs || n_recv_remote % gs)) s_err = 2;
+
+    // ---- phase C: emit the send side (warps 0-1) and the receive side (warps 2-3) ----
+    if (warp < 2) {
+        const int t2 = tid;  // 0..63
+        for (int e = t2; e < E; e += 64) {
+            const int d = e % P, j = e / P;
+            const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
+            const int32_t cnt = T[r * E + e];
+            const int nt = ceil_tiles(cnt);
+            const int32_t pos0 = sp[kd * El + j];
+            const int64_t hrow = d != r ? int64_t(hr[(d * P + r) * El + j] - hr[d * P * El]) : int64_t(rows_in_r + selfo[j]);
+            c.send_first[e] = pos0;
+            for (int ch = 0; ch < nt; ++ch) {
+                const int p = pos0 + ch;
+                if (p >= c.max_send) {
+                    s_err = 3;
+                    break;
+                }
+                SendTile st;
+                st.expert = e;
+                st.dst = d;
+                st.row0 = ch * kTileRows;
+                st.rows = min(kTileRows, cnt - ch * kTileRows);
+                st.heap_row = hrow + int64_t(ch) * kTileRows;
+                st.tile_id = d != r ? tb[r * E + e] + ch : -1;
+                st.group = d == r ? -1 : (gs > 0 ? p / gs : dst_group[d]);
+                st.recv_pos = d == r ? src_first[r] + (rp[j] - rp[0]) + ch : -1;  // self: matching RecvTile
+                st.pad = 0;
+                c.send[p] = st;
+                c.send_done[p] = 0;
+                if (d != r) c.sorder[interleave_pos(dst_n, P, r, d, p - dst_first[d])] = p;
+            }
+        }
+        for (int g = t2; g < n_groups; g += 64) {
+            Group G;
+            if (gs > 0) {
+                G = Group{-1, g * gs, gs, 0};
+            } else {
+                int d = 0;
+                while (dst_group[d] != g) ++d;
+                G = Group{d, dst_first[d], dst_n[d], 0};
+            }
+            c.groups[g] = G;
+            c.group_ctr[g] = 0;
+        }
+    } else {
+        const int t2 = tid - 64;
+        for (int i = t2; i < P * El; i += 64) {
+            const int s = i / El, j = i - s * El, e = r + P * j;
+            const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+            const int32_t cnt = T[s * E + e];
+            const int nt = ceil_tiles(cnt);
+            const int32_t pos0 = rp[ks * El + j];
+            const int64_t hrow = s != r ? int64_t(hr[(r * P + s) * El + j] - hr[r * P * El]) : int64_t(rows_in_r + selfo[j]);
+            for (int ch = 0; ch < nt; ++ch) {
+                const int p = pos0 + ch;
+                if (p >= c.max_recv) {
+                    s_err = 5;
+                    break;
+                }
+                RecvTile rt;
+                rt.src = s;
+                rt.e_local = j;
+                rt.rows = min(kTileRows, cnt - ch * kTileRows);
+                rt.tile_id = s != r ? tb[s * E + e] + ch : -1;
+                rt.heap_row = hrow + int64_t(ch) * kTileRows;
+                rt.ybuf_row = off[s * E + e] + int64_t(ch) * kTileRows;
+                rt.cgroup = s == r ? -1 : (gs > 0 ? (p - n_recv_self) / gs : src_group[s]);
+                rt.pad = 0;
+                c.recv[p] = rt;
+                c.tile_ctr[p] = 0;
+                c.g1_done[p] = 0;
+                // processing order: self tiles first, then remote tiles idx-major over sources
+                c.rorder[s == r ? p : n_recv_self + interleave_pos(src_n, P, r, s, p - src_first[s])] = p;
+            }
+            // M-tile pairs (consecutive chunks of one segment; odd tail paired with -1)
+            for (int pi = 0; 2 * pi < nt; ++pi) {
+                const int q = pp[ks * El + j] + pi;
+                const int po = s == r ? q : src_np[r] + interleave_pos(src_np, P, r, s, q - src_pfirst[s]);
+                if (po < c.max_recv) {
+                    c.pairs[2 * po] = pos0 + 2 * pi;
+                    c.pairs[2 * po + 1] = 2 * pi + 1 < nt ? pos0 + 2 * pi + 1 : -1;
+                }
+            }
+        }
+        for (int g = t2; g < n_cgroups; g += 64) {
+            Group G;
+            if (gs > 0) {
+                G = Group{-1, n_recv_self + g * gs, gs, 0};
+            } else {
+                int s = 0;
+                while (src_group[s] != g) ++s;
+                G = Group{s, src_first[s], src_n[s], 0};
+            }
+            c.cgroups[g] = G;
+            c.cgroup_ctr[g] = 0;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        PlanHeader h;
+        h.n_send = n_send;
+        h.n_send_remote = n_send_remote;
+        h.n_groups = n_groups;
+        h.n_recv = n_recv;
+        h.n_recv_remote = n_recv_remote;
+        h.n_cgroups = n_cgroups;
+        h.total_tiles = s_total_tiles;
+        h.error = s_err;
+        h.n_pairs = n_pairs;
+        h.pad = 0;
+        h.remote_rows_in = rows_in_r;
+        *c.hdr = h;
+        if (s_err) atomicAdd(&c.stats[kStatErrors], 1ull);
+    }
+}
+
+size_t plan4_smem_bytes(const DevCtx& c) { return sizeof(int32_t) * (4 * size_t(c.P) * c.E + 4 * size_t(c.E) + 8); }
+
+cudaError_t configure_plan4(const DevCtx& c) {
+    return cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan4_smem_bytes(c)));
+}
+
+void launch_plan4(const DevCtx& c, cudaStream_t st) { k_plan4<<<1, 128, plan4_smem_bytes(c), st>>>(c); }
+
+}  // namespace perseus
