@@ -184,3 +184,28 @@ def test_fused_kernel_bit_identical_to_stage_kernels(oracle, routing, pair):
         l.close()
     assert np.array_equal(outs[0], outs[1])
     assert cnts[0] == cnts[1]
+
+
+@pytest.mark.parametrize("preset,S,routing", [("llama4-scout", 2048, "balanced"),
+                                               ("deepseek-v3", 1024, "balanced"),
+                                               ("deepseek-v3", 512, "gate")])
+def test_other_baseline_shapes_single_gpu(oracle, preset, S, routing):
+    """BASELINE.json configs[2] (Llama4-Scout: 16 experts top-1, H 5120, ffn 8192)
+    and configs[3] (DeepSeek-V3: 256 experts top-8, H 7168, ffn 2048) on the fused
+    CTA-pair kernel: routing bit-exact, output vs the oracle on a token subset."""
+    import torch
+    from tests.gpu_util import shape_of
+    pb = _pb()
+    m = pb.model_preset(preset)
+    l = pb.MoELayer(m, S, routing=routing, seed=4)
+    x = torch.empty(S, m.hidden_dim, dtype=torch.bfloat16, device="cuda")
+    l.fill_synthetic_x(x, 4)
+    out = torch.empty_like(x)
+    for _ in range(2):
+        l.forward(x, out)
+    torch.cuda.synchronize()
+    c = l.counters()
+    assert c["wait_timeouts"] == 0 and c["errors"] == 0, c
+    subset = np.sort(np.random.default_rng(1).choice(S, 24, replace=False))
+    _check_rank(oracle, pb, shape_of(m, S, 1), l, x, out, routing, 4, 0.0, 0, subset=subset)
+    l.close()
