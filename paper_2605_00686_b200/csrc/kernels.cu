@@ -140,28 +140,24 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
         const int64_t flat = int64_t(t) * c.k + lane;
         my_id = c.routing == PERSEUS_ROUTE_BALANCED ? int(flat % c.E) : c.zipf_ids[flat];
     }
-    float mine = -INFINITY;
     if (lane < c.k) {
-        if (c.routing == PERSEUS_ROUTE_GATE) {
-            mine = l[my_id];
-        } else {
-            // tensor-core router: sum the split-K partial logits in fixed order
-            mine = 0.f;
-            for (int q = 0; q < c.gate_splits; ++q) mine += c.logits[(size_t(q) * c.S + t) * c.E + my_id];
-        }
+        c.ids[size_t(t) * c.k + lane] = my_id;
         // per-256-token-block expert histogram (this forward's parity half)
         atomicAdd(&c.hist[(size_t(c.par) * c.hist_blocks + t / 256) * c.E + my_id], 1);
     }
-    float m = mine;
+    // The combine weights: in the reference routing modes the ids do not depend
+    // on the logits, so the router GEMM runs off the critical path and k_combine
+    // computes the softmax; the learned gate needs the logits here anyway.
+    if (c.routing == PERSEUS_ROUTE_GATE) {
+        const float mine = lane < c.k ? l[my_id] : -INFINITY;
+        float m = mine;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float ex = lane < c.k ? expf(mine - m) : 0.f;
-    float s = ex;
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float ex = lane < c.k ? expf(mine - m) : 0.f;
+        float s = ex;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane < c.k) {
-        c.ids[size_t(t) * c.k + lane] = my_id;
-        c.weights[size_t(t) * c.k + lane] = ex / s;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane < c.k) c.weights[size_t(t) * c.k + lane] = ex / s;
     }
 }
 
@@ -360,6 +356,29 @@ template <int K>
 __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
     const int t = blockIdx.x, v = threadIdx.x;
     const int k = K > 0 ? K : c.k;
+    __shared__ float s_w[16];
+    if (c.routing != PERSEUS_ROUTE_GATE && v < 32) {
+        // softmax over the k chosen experts' logits (tensor-core router: the sum
+        // of the split-K partials in fixed order) — computed here, off the
+        // critical path of the dispatch (k_route no longer waits for the router)
+        float mine = -INFINITY;
+        if (v < k) {
+            const int e = c.ids[size_t(t) * k + v];
+            mine = 0.f;
+            for (int q = 0; q < c.gate_splits; ++q) mine += c.logits[(size_t(q) * c.S + t) * c.E + e];
+        }
+        float m = mine;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float ex = v < k ? expf(mine - m) : 0.f;
+        float s = ex;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (v < k) {
+            s_w[v] = ex / s;
+            c.weights[size_t(t) * k + v] = ex / s;
+        }
+    }
     if (c.P > 1 && v < k) {
         const int e = c.ids[size_t(t) * k + v];
         if (e % c.P != c.rank) {
@@ -378,7 +397,7 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
     for (int j = 0; j < KM; ++j) {
         if (j < k) {
             const int32_t p = c.pos[size_t(t) * k + j];
-            w[j] = c.weights[size_t(t) * k + j];
+            w[j] = c.routing != PERSEUS_ROUTE_GATE ? s_w[j] : c.weights[size_t(t) * k + j];
             u[j] = *reinterpret_cast<const uint4*>(y + size_t(p) * c.H + v * 8);
         }
     }

@@ -103,6 +103,8 @@ struct perseus_layer {
     int num_sms = 148;
     uint32_t epoch = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;                      // router GEMM side stream
+    cudaEvent_t ev_x = nullptr, ev_gate = nullptr;
 
     // local
     bf16 *x_stage = nullptr, *out_stage = nullptr;
@@ -218,6 +220,9 @@ void free_layer(perseus_layer* L) {
     for (auto& e : L->ev)
         if (e) cudaEventDestroy(e);
     if (L->stream) cudaStreamDestroy(L->stream);
+    if (L->stream2) cudaStreamDestroy(L->stream2);
+    if (L->ev_x) cudaEventDestroy(L->ev_x);
+    if (L->ev_gate) cudaEventDestroy(L->ev_gate);
     delete L;
 }
 
@@ -234,9 +239,18 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     }
     const bool all = phase == PERSEUS_PHASE_ALL;
     if (all) ck(cudaEventRecord(L->ev[0], st), "event");
+    // Reference routing modes: the expert ids do not depend on the logits, so the
+    // router GEMM runs on a side stream, overlapped with route/permute/plan, and
+    // only the weights (computed in the combine) wait for it.
+    const bool side_gate = all && L->fused && L->cfg.routing != PERSEUS_ROUTE_GATE;
     if (all || phase == PERSEUS_PHASE_ROUTE) {
         if (L->cfg.routing == PERSEUS_ROUTE_GATE) {
             launch_gate_exact(c, st);  // bit-exact fp32 order: learned top-k ids must match the oracle
+        } else if (side_gate) {
+            ck(cudaEventRecord(L->ev_x, st), "event");
+            ck(cudaStreamWaitEvent(L->stream2, L->ev_x, 0), "wait");
+            launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, L->stream2);
+            ck(cudaEventRecord(L->ev_gate, L->stream2), "event");
         } else {
             launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, st);
         }
@@ -247,6 +261,7 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         // one persistent kernel: dispatch puts + GEMM1 + GEMM2/combine puts,
         // overlapped tile by tile (gemm.cu:k_moe)
         launch_plan(c, st);
+        if (side_gate) ck(cudaStreamWaitEvent(st, L->ev_gate, 0), "wait");  // router done before the persistent kernel
         ck(cudaEventRecord(L->ev[2], st), "event");
         if (L->pair)
             ck(launch_moe2(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
@@ -308,6 +323,9 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             ck(cudaSetDevice(device), "cudaSetDevice");
             ck(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
             ck(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&L->stream2, cudaStreamNonBlocking), "stream2");
+            ck(cudaEventCreateWithFlags(&L->ev_x, cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&L->ev_gate, cudaEventDisableTiming), "event");
             for (auto& e : L->ev) ck(cudaEventCreate(&e), "event");
 
             const size_t H = L->H, I = L->I, E = L->E, El = L->El, S = L->S, P = world;

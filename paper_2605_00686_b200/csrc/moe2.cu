@@ -44,6 +44,7 @@ constexpr int kStgBytes = 128 * kStgRow;
 constexpr int kRing = 8;
 constexpr int kUnitRows = 2;  // fine units: few tiles in flight, so tiles land one after another at link rate
 constexpr int kUnitsPerTile = kTileRows / kUnitRows;
+constexpr int kSelfWindow = 160;  // self tiles (x 512 KB at H=2048) copied ahead of consumption
 constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 
 struct Args {
@@ -291,6 +292,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 other_done = true;
                 remote_q = !remote_q;
                 continue;
+            }
+            if (!remote_q) {
+                // Pace the self copies: stay at most kSelfWindow tiles ahead of the
+                // tiles the scheduler has handed out, so heap rows are still in L2
+                // when GEMM1 reads them (self tiles are consumed first, in this
+                // order).  The items of every grabbed tile are always allowed.
+                const int need = u / kUnitsPerTile;
+                if (lane == 0) {
+                    while (true) {
+                        const int w = int(*reinterpret_cast<volatile uint32_t*>(c.sched));
+                        const int L = min(f.lag, T);
+                        const int started = w < L * f.n1 ? w / f.n1 : L + (w - L * f.n1) / (f.n1 + f.n2);
+                        if (need < 2 * started + kSelfWindow) break;
+                        __nanosleep(256);
+                    }
+                }
+                __syncwarp();
             }
             const int sp = remote_q ? c.sorder[u / kUnitsPerTile] : hdr.n_send_remote + u / kUnitsPerTile;
             const SendTile st = c.send[sp];
