@@ -210,6 +210,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="stage kernels instead of the fused persistent kernel")
     ap.add_argument("--no-pair", action="store_true", help="fused kernel on single CTAs instead of CTA pairs")
+    ap.add_argument("--variant-steps", type=int, default=200,
+                    help="N>1: also time the per-tile-fence (vanilla) variant of the same kernel for this many steps")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3  # timing rule: W >= 3
@@ -283,11 +285,24 @@ def main():
 
     # ---- per-stage times (CUDA events inside the layer, on its stream) ----
     stages = []
+    layer.set_stage_timing(True)  # outside the timed region
     for _ in range(min(args.steps, 10)):
         layer.forward(x, out)
         stages.append(layer.timing())
     stages = np.array(stages)
     st_mean = stages.mean(0).tolist()  # [route, dispatch, gemm1, gemm2, combine] ms
+    layer.set_stage_timing(False)
+    # ---- per-kernel device timeline (globaltimer), outside the timed region ----
+    layer.set_timeline(True)
+    tls = []
+    for _ in range(min(args.steps, 10)):
+        layer.forward(x, out)
+        torch.cuda.synchronize()
+        tls.append(layer.timeline())
+    layer.set_timeline(False)
+    timeline_us = {kname: [round(float(np.mean([tl[kname][0] for tl in tls])) / 1e3, 1),
+                           round(float(np.mean([tl[kname][1] for tl in tls])) / 1e3, 1)]
+                   for kname in tls[0] if all(kname in tl and tl[kname][1] is not None for tl in tls)}
 
     # ---- end-to-end through the public host API: H2D x, forward, D2H out ----
     x_host = torch.empty(S, H, dtype=torch.int16).pin_memory()
@@ -310,6 +325,32 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * S * args.steps / float(te.item())
+
+    # ---- the per-tile-fence variant of the same kernel (N > 1) ----
+    variant = None
+    if world > 1 and args.variant_steps > 0 and args.signaling != "vanilla":
+        vl = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing, skew=args.skew,
+                         seed=1, protocol=pb.vanilla_protocol(), fused=not args.unfused, pair=not args.no_pair)
+        vl.connect_dist()
+        for _ in range(args.warmup):
+            vl.forward(x, out)
+        barrier()
+        v0 = vl.counters()
+        vs, ve = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        vs.record(stream)
+        for _ in range(args.variant_steps):
+            vl.forward(x, out)
+        ve.record(stream)
+        barrier()
+        v1 = vl.counters()
+        vt = torch.tensor([vs.elapsed_time(ve)], device="cuda")
+        dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+        v_ms = float(vt.item()) / args.variant_steps
+        vd = {key: (v1[key] - v0[key]) / args.variant_steps for key in ("dispatch_fences", "combine_fences")}
+        variant = {"signaling": "coupled (per-tile fence), same fused kernel", "steps": args.variant_steps,
+                   "ms_per_step": v_ms, "value": world * S / (v_ms / 1e3), "unit": "tokens/s",
+                   "fences_per_forward": vd}
+        vl.close()
     clk.__exit__(None, None, None)
 
     # ---- roofline of the dominant kernel ----
@@ -373,7 +414,36 @@ def main():
         dc["frac_wait_dispatch"] = dc["wait_dispatch_ns"] / dc["cta_ns"]
         dc["frac_wait_g1"] = dc["wait_g1_ns"] / dc["cta_ns"]
         dc["frac_copy_busy"] = dc["copy_ns"] / ((6 if not args.no_pair else 2) * dc["cta_ns"])
-    launches_per_step = 10
+    if dc.get("mma_cycles"):
+        # MMA issuer (leader CTA of each pair): where the tensor pipe's feeder waits
+        for key in ("mma_ring_wait", "mma_acc_wait", "mma_data_wait"):
+            dc["frac_" + key] = dc[key] / dc["mma_cycles"]
+    comm = None
+    if world > 1 and not args.unfused:
+        # communication evidence from the device's own timestamps (globaltimer):
+        # achieved NVLink GB/s of the remote dispatch / combine stores over their
+        # active spans, and EXPOSED communication = time the GEMM pipeline sat
+        # waiting for remote tiles (producer, mean over CTAs) + combine kernel
+        # start -> last combine flag
+        n_cta = torch.cuda.get_device_properties(local).multi_processor_count & ~1
+        exp_d = dc["wait_remote_ns"] / n_cta / 1e3
+        exp_c = dc["combine_wait_ns"] / 1e3
+        comm = {"dispatch_nvlink_gbs": dc["dispatch_put_bytes"] / dc["dispatch_span_ns"] if dc["dispatch_span_ns"] else None,
+                "combine_nvlink_gbs": dc["combine_put_bytes"] / dc["combine_span_ns"] if dc["combine_span_ns"] else None,
+                "dispatch_span_us": dc["dispatch_span_ns"] / 1e3, "combine_span_us": dc["combine_span_ns"] / 1e3,
+                "dispatch_bytes": dc["dispatch_put_bytes"], "combine_bytes": dc["combine_put_bytes"],
+                "exposed_dispatch_us": exp_d, "exposed_combine_us": exp_c,
+                "exposed_frac": (exp_d + exp_c) / (ms_step * 1e3),
+                "fences_per_forward": {"dispatch": dc["dispatch_fences"], "combine": dc["combine_fences"]},
+                "note": "rank 0's device counters; spans are first remote store -> last remote tile signalled"}
+    if variant is not None and dc.get("dispatch_fences"):
+        variant["fence_ratio_vs_this_run"] = {
+            "dispatch": variant["fences_per_forward"]["dispatch_fences"] / dc["dispatch_fences"],
+            "combine": variant["fences_per_forward"]["combine_fences"] / max(dc["combine_fences"], 1e-9)}
+        variant["slowdown_vs_this_run"] = variant["ms_per_step"] / ms_step
+    # our kernels per forward: router GEMM, k_route, k_perm, k_plan4, then k_moe2 (fused)
+    # or k_dispatch + k_gemm<1> + k_gemm<2> (unfused), then k_combine
+    launches_per_step = 6 if not args.unfused else 8
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -392,6 +462,7 @@ def main():
                                   "combine"] if args.unfused else
                                  ["route_permute", "plan", "fused_dispatch_ffn_combineput", "-", "combine"],
                                  st_mean)),
+            "timeline_us": timeline_us,
             "fused": not args.unfused,
             "cta_pairs": not args.no_pair and not args.unfused,
             "group_size": args.group_size,
@@ -401,6 +472,8 @@ def main():
                                "t_nvlink_us": nvl_bytes / 770e9 * 1e6,
                                "t_hbm_us": hbm_layer / (hbm_peak * 1e9) * 1e6},
             "roofline": roof,
+            "comm": comm,
+            "per_tile_fence_variant": variant,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": S * H * 2,
                     "d2h_bytes_per_step": S * H * 2,
                     "ms_per_step": 1e3 * float(te.item()) / args.steps},

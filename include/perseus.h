@@ -194,6 +194,14 @@ typedef struct perseus_counters {
     int64_t wait_g1_ns;            /* ... producer blocked on GEMM1->GEMM2 tile dependencies */
     int64_t copy_ns;               /* ... copy warps busy with dispatch puts */
     int64_t cta_ns;                /* ... CTA lifetimes (normaliser) */
+    int64_t wait_remote_ns;        /* ... producer blocked on REMOTE dispatch flags (exposed dispatch) */
+    int64_t dispatch_span_ns;      /* per forward, summed: first remote dispatch store -> last tile signalled */
+    int64_t combine_span_ns;       /* ... first remote combine store -> last combine tile signalled */
+    int64_t combine_wait_ns;       /* ... longest wait of a combine CTA for its combine flags (exposed combine) */
+    int64_t mma_cycles;            /* CTA-pair kernel, MMA issuers, SM cycles in the issue loop (summed) */
+    int64_t mma_ring_wait;         /* ... of which waiting for the next work item */
+    int64_t mma_acc_wait;          /* ... waiting for a free TMEM accumulator (epilogue back-pressure) */
+    int64_t mma_data_wait;         /* ... waiting for TMA operand stages */
 } perseus_counters;
 int perseus_layer_counters(perseus_layer* layer, perseus_counters* out);
 
@@ -214,9 +222,21 @@ int perseus_layer_read_layout(perseus_layer* layer, perseus_transfer* sent, size
 /* The count table [P][E] this rank received from all ranks in the last forward. */
 int perseus_layer_read_count_table(perseus_layer* layer, int32_t* table);
 
+/* Kernel timeline of every following forward (diagnostics): globaltimer ns
+ * [start, end] per kernel in the order router GEMM, route, permute, plan,
+ * fused kernel, combine, dispatch, GEMM1, GEMM2 (0 = did not run).  Start =
+ * first CTAs after their dependency wait, end = last CTAs. */
+int perseus_layer_set_timeline(perseus_layer* layer, int on);
+int perseus_layer_read_timeline(perseus_layer* layer, uint64_t* start_end, int n_kernels);
+
+/* Record per-stage CUDA events in every following forward (off by default: each
+ * event record costs stream time). */
+int perseus_layer_set_stage_timing(perseus_layer* layer, int on);
+
 /* Timing of the stages of the last perseus_layer_forward, in ms (CUDA events on
  * its stream): [route+permute, plan+dispatch, GEMM1+SwiGLU, GEMM2+combine-put,
- * combine]. */
+ * combine].  Fused path: [route+permute, plan, fused kernel, -, combine].
+ * Config error unless stage timing was on for that forward. */
 int perseus_layer_read_timing(perseus_layer* layer, float* ms, int n);
 
 #ifdef __cplusplus

@@ -49,7 +49,9 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "epoch", "dispatch_fences", "dispatch_signals", "dispatch_puts", "dispatch_put_bytes",
         "combine_fences", "combine_signals", "combine_puts", "combine_put_bytes", "recv_tiles",
-        "wait_timeouts", "errors", "wait_dispatch_ns", "wait_g1_ns", "copy_ns", "cta_ns")]
+        "wait_timeouts", "errors", "wait_dispatch_ns", "wait_g1_ns", "copy_ns", "cta_ns",
+        "wait_remote_ns", "dispatch_span_ns", "combine_span_ns", "combine_wait_ns",
+        "mma_cycles", "mma_ring_wait", "mma_acc_wait", "mma_data_wait")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -90,6 +92,9 @@ def _load():
         "perseus_layer_read_layout": (C.c_int, [vp, P(Transfer), sz, P(sz), P(i64), sz, P(sz)]),
         "perseus_layer_read_count_table": (C.c_int, [vp, P(i32)]),
         "perseus_layer_read_timing": (C.c_int, [vp, P(C.c_float), C.c_int]),
+        "perseus_layer_set_stage_timing": (C.c_int, [vp, C.c_int]),
+        "perseus_layer_set_timeline": (C.c_int, [vp, C.c_int]),
+        "perseus_layer_read_timeline": (C.c_int, [vp, P(C.c_uint64), C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

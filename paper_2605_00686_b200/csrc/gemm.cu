@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
+    constexpr int kTlId = kMode == 0 ? kTlGate : (kMode == 1 ? kTlGemm1 : kTlGemm2);
+    tl_start(c, kTlId);
     int total;
     if (kMode == 0) {
         total = g.n_tiles;
@@ -349,6 +351,7 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    tl_end(c, kTlId, threadIdx.x == 0);
     if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
 }
 
@@ -597,6 +600,9 @@ __global__ void __launch_bounds__(256, 1)
             publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
                                 kStatDispatchFences, kStatDispatchSignals);
         }
+        // the routing weights (router GEMM ran on a side stream), after the puts
+        if (c.weights_late)
+            for (int t = blockIdx.x * 2 + (warp - 2); t < c.S; t += gridDim.x * 2) route_weights_warp(c, t, lane);
     } else {
         // ---------------- epilogue (4 warps = 4 TMEM lane quadrants) ----------------
         const int q = warp & 3;

@@ -5,16 +5,20 @@
 // The grouped expert FFN (tcgen05) is in gemm.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "layer_dev.h"
 #include "perseus.h"
 #include "ptx.cuh"
 #include "signal.cuh"
+#include "plan.cuh"
 
 namespace perseus {
 
 using namespace ptx;
 
 size_t perm_smem_bytes(const DevCtx& c);
+
 
 // ------------------------------------------------------------ synthetic ----
 // Same counter hash as oracle/oracle.c:orc_fill_bf16 (bit-identical bf16).
@@ -104,6 +108,9 @@ __global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const 
 //   BALANCED : id[t*k+j] = (t*k+j) mod E (exact capacity, workload.cpp:180-195)
 //   ZIPF     : the reference's Zipf draws (workload.cpp:57-97), host-expanded
 __global__ void __launch_bounds__(256) k_route(DevCtx c) {
+    pdl_wait();
+    pdl_launch_dependents();
+    tl_start(c, kTlRoute);
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (t >= c.S) return;
@@ -145,9 +152,10 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
         // per-256-token-block expert histogram (this forward's parity half)
         atomicAdd(&c.hist[(size_t(c.par) * c.hist_blocks + t / 256) * c.E + my_id], 1);
     }
-    // The combine weights: in the reference routing modes the ids do not depend
-    // on the logits, so the router GEMM runs off the critical path and k_combine
-    // computes the softmax; the learned gate needs the logits here anyway.
+    // The routing weights.  Learned gate: from the exact logits.  Reference
+    // routing modes: the ids do not depend on the logits; when the router GEMM
+    // ran on a side stream (fused path) the fused kernel's copy warps write the
+    // weights, otherwise the split-K partials are already summable here.
     if (c.routing == PERSEUS_ROUTE_GATE) {
         const float mine = lane < c.k ? l[my_id] : -INFINITY;
         float m = mine;
@@ -158,7 +166,11 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane < c.k) c.weights[size_t(t) * c.k + lane] = ex / s;
+    } else if (!c.weights_late) {
+        __syncwarp();
+        route_weights_warp(c, t, lane);
     }
+    tl_end(c, kTlRoute, threadIdx.x == 0);
 }
 
 // ----------------------------------------------------------- permutation ----
@@ -183,6 +195,9 @@ __global__ void __launch_bounds__(kPermT) k_hist(DevCtx c) {
 __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33*/);
 
 __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
+    pdl_wait();
+    pdl_launch_dependents();
+    tl_start(c, kTlPerm);
     extern __shared__ int32_t sm[];
     const int E = c.E, b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
     uint32_t* bits = reinterpret_cast<uint32_t*>(sm);  // [E][kPermT / 32]
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     __syncthreads();
     if (b == 0 && tid == 0) {
         // one sys-scope fence, then the per-source ready flag at every PE
-        fence_acq_rel_sys();
+        if (c.P > 1) fence_acq_rel_sys();  // P == 1: the plan kernel is stream-ordered after this one
         for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
     }
     const int32_t total = block_exclusive_scan(tot, E, scratch);
@@ -238,21 +253,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         c.rows[p] = t;
         c.pos[size_t(t) * c.k + j] = p;
     }
-}
-
-// -------------------------------------------------------- count exchange ----
-// Publish this rank's per-expert counts into every PE's count table (peer
-// stores), one sys-scope fence, then the per-source ready flags.
-__global__ void __launch_bounds__(256) k_publish_counts(DevCtx c) {
-    for (int p = 0; p < c.P; ++p) {
-        int32_t* dst = c.count_table[p] + (size_t(c.par) * c.P + c.rank) * c.E;
-        for (int e = threadIdx.x; e < c.E; e += blockDim.x) dst[e] = c.counts[e];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        fence_acq_rel_sys();
-        for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
-    }
+    tl_end(c, kTlPerm, tid == 0);
 }
 
 // ------------------------------------------------------------------ plan ----
@@ -307,6 +308,7 @@ __device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTi
 // peer, a local copy for the self segment — then signal (Phase 1: counter;
 // the completing producer runs Phase 2).
 __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
+    tl_start(c, kTlDispatch);
     const PlanHeader hdr = *c.hdr;
     const int i = blockIdx.x;
     if (i >= hdr.n_send || hdr.error) return;
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
         }
         for (; v < nvec; v += 32) dst[v] = __ldg(src + v);
     }
+    if (c.tl && threadIdx.x == 0 && i + 4 >= hdr.n_send) atomicMax(c.tl + 2 * kTlDispatch + 1, fwd_now());
     if (st.dst == c.rank) return;  // self segment: ordered by the stream, no signal
     __syncthreads();
     if (warp != 0) return;
@@ -354,31 +357,12 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
 // sorted slot p is send tile send_first[e] + (p - offsets[e]) / 128.
 template <int K>
 __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
+    pdl_wait();
+    tl_start(c, kTlCombine);
     const int t = blockIdx.x, v = threadIdx.x;
     const int k = K > 0 ? K : c.k;
-    __shared__ float s_w[16];
-    if (c.routing != PERSEUS_ROUTE_GATE && v < 32) {
-        // softmax over the k chosen experts' logits (tensor-core router: the sum
-        // of the split-K partials in fixed order) — computed here, off the
-        // critical path of the dispatch (k_route no longer waits for the router)
-        float mine = -INFINITY;
-        if (v < k) {
-            const int e = c.ids[size_t(t) * k + v];
-            mine = 0.f;
-            for (int q = 0; q < c.gate_splits; ++q) mine += c.logits[(size_t(q) * c.S + t) * c.E + e];
-        }
-        float m = mine;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const float ex = v < k ? expf(mine - m) : 0.f;
-        float s = ex;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (v < k) {
-            s_w[v] = ex / s;
-            c.weights[size_t(t) * k + v] = ex / s;
-        }
-    }
+    uint64_t t_start = 0;
+    if (c.P > 1 && v == 0) t_start = fwd_now();
     if (c.P > 1 && v < k) {
         const int e = c.ids[size_t(t) * k + v];
         if (e % c.P != c.rank) {
@@ -389,6 +373,20 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
         }
     }
     __syncthreads();
+    if (c.P > 1 && v == 0) {
+        // exposed-communication accounting: the longest any CTA waited for its
+        // combine flags; the last CTA folds this forward's timestamps into the stats
+        atomicMax(c.fwd_t + kFwdWaitMax, fwd_now() - t_start);
+        __threadfence();
+        if (atomicAdd(c.fwd_t + kFwdDoneCtas, 1ull) == gridDim.x - 1) {
+            __threadfence();
+            volatile unsigned long long* ft = c.fwd_t;
+            auto span = [&](int a, int b) { return ft[b] > ft[a] && ft[a] != ~0ull ? ft[b] - ft[a] : 0ull; };
+            atomicAdd(&c.stats[kStatDispatchSpanNs], span(kFwdDispFirst, kFwdDispLast));
+            atomicAdd(&c.stats[kStatCombineSpanNs], span(kFwdCombFirst, kFwdCombLast));
+            atomicAdd(&c.stats[kStatCombineWaitNs], ft[kFwdWaitMax]);
+        }
+    }
     const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
     constexpr int KM = K > 0 ? K : 16;
     uint4 u[KM];
@@ -397,7 +395,7 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
     for (int j = 0; j < KM; ++j) {
         if (j < k) {
             const int32_t p = c.pos[size_t(t) * k + j];
-            w[j] = c.routing != PERSEUS_ROUTE_GATE ? s_w[j] : c.weights[size_t(t) * k + j];
+            w[j] = c.weights[size_t(t) * k + j];
             u[j] = *reinterpret_cast<const uint4*>(y + size_t(p) * c.H + v * 8);
         }
     }
@@ -416,6 +414,7 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
     o.z = pack_bf16(acc[4], acc[5]);
     o.w = pack_bf16(acc[6], acc[7]);
     *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + v * 8) = o;
+    tl_end(c, kTlCombine, v == 0);
 }
 
 // ------------------------------------------------------------- launchers ----
@@ -425,21 +424,30 @@ void launch_gate_exact(const DevCtx& c, cudaStream_t st) {
     k_gate<<<g, 256, 0, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
 }
 
+// the per-forward plan (plan.cuh), one CTA of 4 warps
+__global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (c.tl && threadIdx.x == 0) atomicMax(c.tl + 2 * kTlPlan, ~fwd_now());
+    extern __shared__ int32_t sm[];
+    plan_body(c, sm);
+    if (c.tl && threadIdx.x == 0) atomicMax(c.tl + 2 * kTlPlan + 1, fwd_now());
+}
+
 // route + permutation + count publish (after the gate logits exist)
 void launch_route(const DevCtx& c, cudaStream_t st) {
-    k_route<<<(c.S + 7) / 8, 256, 0, st>>>(c);  // + block histograms
+    launch_pdl(k_route, dim3((c.S + 7) / 8), dim3(256), 0, st, c);  // + block histograms
     const int nb = (c.S + kPermT - 1) / kPermT;
-    k_perm<<<nb, kPermT, perm_smem_bytes(c), st>>>(c);  // + count publish
+    launch_pdl(k_perm, dim3(nb), dim3(kPermT), perm_smem_bytes(c), st, c);  // + count publish
 }
 
 size_t perm_smem_bytes(const DevCtx& c) {
     return sizeof(int32_t) * (size_t(c.E) * (kPermT / 32) + 2 * size_t(c.E) + 40);
 }
 
-
-void launch_plan4(const DevCtx& c, cudaStream_t st);
-cudaError_t configure_plan4(const DevCtx& c);
-void launch_plan(const DevCtx& c, cudaStream_t st) { launch_plan4(c, st); }
+void launch_plan(const DevCtx& c, cudaStream_t st) {
+    launch_pdl(k_plan4, dim3(1), dim3(128), plan_smem_bytes(c), st, c);
+}
 
 void launch_dispatch(const DevCtx& c, cudaStream_t st) {
     launch_plan(c, st);
@@ -449,18 +457,35 @@ void launch_dispatch(const DevCtx& c, cudaStream_t st) {
 void launch_combine(const DevCtx& c, cudaStream_t st) {
     const int threads = c.H / 8;  // H <= 8192
     switch (c.k) {
-        case 1: k_combine<1><<<c.S, threads, 0, st>>>(c); break;
-        case 2: k_combine<2><<<c.S, threads, 0, st>>>(c); break;
-        case 4: k_combine<4><<<c.S, threads, 0, st>>>(c); break;
-        case 8: k_combine<8><<<c.S, threads, 0, st>>>(c); break;
-        default: k_combine<0><<<c.S, threads, 0, st>>>(c); break;
+        case 1: launch_pdl(k_combine<1>, dim3(c.S), dim3(threads), 0, st, c); break;
+        case 2: launch_pdl(k_combine<2>, dim3(c.S), dim3(threads), 0, st, c); break;
+        case 4: launch_pdl(k_combine<4>, dim3(c.S), dim3(threads), 0, st, c); break;
+        case 8: launch_pdl(k_combine<8>, dim3(c.S), dim3(threads), 0, st, c); break;
+        default: launch_pdl(k_combine<0>, dim3(c.S), dim3(threads), 0, st, c); break;
     }
 }
 
+// Every kernel of the forward asks for the maximum shared-memory carveout, so
+// consecutive kernels never wait for an SM to drain and re-split L1/smem (the
+// fused and GEMM kernels need it anyway).
+template <typename K>
+static cudaError_t max_carveout(K* kernel) {
+    return cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                int(cudaSharedmemCarveoutMaxShared));
+}
+
 cudaError_t configure_kernels(const DevCtx& c) {
-    cudaError_t e = configure_plan4(c);
+    cudaError_t e = cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan_smem_bytes(c)));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(perm_smem_bytes(c)));
+    e = cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(perm_smem_bytes(c)));
+    if (e != cudaSuccess) return e;
+    const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_perm), max_carveout(k_plan4), max_carveout(k_dispatch),
+                              max_carveout(k_gate), max_carveout(k_synth_fill), max_carveout(k_combine<0>),
+                              max_carveout(k_combine<1>), max_carveout(k_combine<2>), max_carveout(k_combine<4>),
+                              max_carveout(k_combine<8>)};
+    for (cudaError_t x : es)
+        if (x != cudaSuccess) return x;
+    return cudaSuccess;
 }
 
 }  // namespace perseus

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,8 +25,8 @@ void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, flo
 void launch_gate_exact(const DevCtx& c, cudaStream_t st);
 void launch_gate_tc(const CUtensorMap& tx, const CUtensorMap& twg, const DevCtx& c, int grid, cudaStream_t st);
 void launch_route(const DevCtx& c, cudaStream_t st);
-void launch_dispatch(const DevCtx& c, cudaStream_t st);
 void launch_plan(const DevCtx& c, cudaStream_t st);
+void launch_dispatch(const DevCtx& c, cudaStream_t st);
 cudaError_t configure_moe();
 cudaError_t configure_moe2();
 cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
@@ -119,8 +120,11 @@ struct perseus_layer {
     uint32_t *group_ctr = nullptr, *cgroup_ctr = nullptr, *tile_ctr = nullptr;
     int32_t *sorder = nullptr, *rorder = nullptr;
     uint32_t *send_done = nullptr, *g1_done = nullptr, *self_ready = nullptr, *sched = nullptr;
+    unsigned long long* fwd_t = nullptr;
+    unsigned long long* tl = nullptr;  // kernel timeline (perseus_layer_set_timeline)
     int32_t* send_first = nullptr;
     bool fused = true;  // forward() uses the fused persistent kernel
+    bool stage_timing = false, timed_last = false;  // per-stage CUDA events (perseus_layer_set_stage_timing)
     bool pair = true;   // ... on CTA pairs (cta_group::2)
     int32_t* pairs = nullptr;
     unsigned long long* stats = nullptr;
@@ -167,7 +171,7 @@ struct perseus_layer {
         c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
         c.max_send = max_send; c.max_recv = max_recv;
         c.sorder = sorder; c.rorder = rorder; c.send_done = send_done; c.g1_done = g1_done;
-        c.self_ready = self_ready; c.sched = sched; c.send_first = send_first; c.pairs = pairs;
+        c.self_ready = self_ready; c.sched = sched; c.fwd_t = fwd_t; c.tl = tl; c.send_first = send_first; c.pairs = pairs;
         c.stats = stats;
         return c;
     }
@@ -213,7 +217,7 @@ void free_layer(perseus_layer* L) {
     void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
-                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched,
+                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl,
                     L->send_first, L->pairs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -238,11 +242,25 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         L->tm_x_ptr = c.x;
     }
     const bool all = phase == PERSEUS_PHASE_ALL;
-    if (all) ck(cudaEventRecord(L->ev[0], st), "event");
+    // stage events only when asked for (each record costs ~1-3 us of stream time)
+    const bool tev = all && L->stage_timing;
+    if (all) L->timed_last = tev;
+    if (tev) ck(cudaEventRecord(L->ev[0], st), "event");
+    if (all && L->tl) ck(cudaMemsetAsync(L->tl, 0, 2 * kTlCount * sizeof(unsigned long long), st), "memset");
     // Reference routing modes: the expert ids do not depend on the logits, so the
     // router GEMM runs on a side stream, overlapped with route/permute/plan, and
-    // only the weights (computed in the combine) wait for it.
-    const bool side_gate = all && L->fused && L->cfg.routing != PERSEUS_ROUTE_GATE;
+    // only the routing weights (written by the fused kernel) wait for it.
+    static const bool side_ok = [] { const char* e = getenv("PERSEUS_SIDE_GATE"); return !e || atoi(e) != 0; }();
+    const bool side_gate = side_ok && all && L->fused && L->cfg.routing != PERSEUS_ROUTE_GATE;
+    c.weights_late = side_gate;
+    // pair order: the first ~two waves of GEMM1 items on self pairs, then the
+    // remote pairs (same lag as launch_moe2's item interleave)
+    c.self_head = std::max(1, (L->num_sms + L->I / 128 - 1) / (L->I / 128));
+    {
+        const double t_tile = 128.0 * L->H * 2 / 600e9;                   // NVLink store rate per sender
+        const double t_pair = 2.0 * 128 * 6.0 * L->H * L->I / 1.0e15;      // GPU-wide: pairs complete at ~1 PFLOP/s
+        c.head_ratio = float(t_tile / t_pair);
+    }
     if (all || phase == PERSEUS_PHASE_ROUTE) {
         if (L->cfg.routing == PERSEUS_ROUTE_GATE) {
             launch_gate_exact(c, st);  // bit-exact fp32 order: learned top-k ids must match the oracle
@@ -256,36 +274,36 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         }
         launch_route(c, st);
     }
-    if (all) ck(cudaEventRecord(L->ev[1], st), "event");
+    if (tev) ck(cudaEventRecord(L->ev[1], st), "event");
     if (all && L->fused) {
+        launch_plan(c, st);
         // one persistent kernel: dispatch puts + GEMM1 + GEMM2/combine puts,
         // overlapped tile by tile (gemm.cu:k_moe)
-        launch_plan(c, st);
         if (side_gate) ck(cudaStreamWaitEvent(st, L->ev_gate, 0), "wait");  // router done before the persistent kernel
-        ck(cudaEventRecord(L->ev[2], st), "event");
+        if (tev) ck(cudaEventRecord(L->ev[2], st), "event");
         if (L->pair)
             ck(launch_moe2(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
                "launch k_moe2");
         else
             ck(launch_moe(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
                "launch k_moe");
-        ck(cudaEventRecord(L->ev[3], st), "event");
-        ck(cudaEventRecord(L->ev[4], st), "event");
+        if (tev) ck(cudaEventRecord(L->ev[3], st), "event");
+        if (tev) ck(cudaEventRecord(L->ev[4], st), "event");
         launch_combine(c, st);
-        ck(cudaEventRecord(L->ev[5], st), "event");
+        if (tev) ck(cudaEventRecord(L->ev[5], st), "event");
         ck(cudaGetLastError(), "kernel launch");
         return;
     }
     if (all || phase == PERSEUS_PHASE_DISPATCH) launch_dispatch(c, st);
-    if (all) ck(cudaEventRecord(L->ev[2], st), "event");
+    if (tev) ck(cudaEventRecord(L->ev[2], st), "event");
     if (all || phase == PERSEUS_PHASE_EXPERT) {
         launch_gemm(1, L->tm_a1, L->tm_b1, c, L->I / 128, L->H / 64, int64_t(c.par) * L->R_max, L->num_sms, st);
-        if (all) ck(cudaEventRecord(L->ev[3], st), "event");
+        if (tev) ck(cudaEventRecord(L->ev[3], st), "event");
         launch_gemm(2, L->tm_a2, L->tm_b2, c, L->H / 256, L->I / 64, 0, L->num_sms, st);
     }
-    if (all) ck(cudaEventRecord(L->ev[4], st), "event");
+    if (tev) ck(cudaEventRecord(L->ev[4], st), "event");
     if (all || phase == PERSEUS_PHASE_COMBINE) launch_combine(c, st);
-    if (all) ck(cudaEventRecord(L->ev[5], st), "event");
+    if (tev) ck(cudaEventRecord(L->ev[5], st), "event");
     ck(cudaGetLastError(), "kernel launch");
 }
 
@@ -360,6 +378,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->g1_done = dalloc<uint32_t>(L->max_recv);
             L->self_ready = dalloc<uint32_t>(L->max_recv);
             L->sched = dalloc<uint32_t>(4);
+            L->fwd_t = dalloc<unsigned long long>(kFwdSlots);
             L->send_first = dalloc<int32_t>(E);
             L->pairs = dalloc<int32_t>(2 * size_t(L->max_recv) + 4);
             L->stats = dalloc<unsigned long long>(kStatCount);
@@ -534,6 +553,14 @@ int perseus_layer_counters(perseus_layer* L, perseus_counters* out) {
         out->wait_g1_ns = int64_t(s[kStatWaitG1Ns]);
         out->copy_ns = int64_t(s[kStatCopyNs]);
         out->cta_ns = int64_t(s[kStatCtaNs]);
+        out->wait_remote_ns = int64_t(s[kStatWaitRemoteNs]);
+        out->dispatch_span_ns = int64_t(s[kStatDispatchSpanNs]);
+        out->combine_span_ns = int64_t(s[kStatCombineSpanNs]);
+        out->combine_wait_ns = int64_t(s[kStatCombineWaitNs]);
+        out->mma_cycles = int64_t(s[kStatMmaCycles]);
+        out->mma_ring_wait = int64_t(s[kStatMmaRingWait]);
+        out->mma_acc_wait = int64_t(s[kStatMmaAccWait]);
+        out->mma_data_wait = int64_t(s[kStatMmaDataWait]);
     });
 }
 
@@ -591,8 +618,39 @@ int perseus_layer_read_count_table(perseus_layer* L, int32_t* table) {
     });
 }
 
+int perseus_layer_set_timeline(perseus_layer* L, int on) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        if (on && !L->tl) {
+            ck(cudaMalloc(&L->tl, 2 * kTlCount * sizeof(unsigned long long)), "cudaMalloc");
+            ck(cudaMemset(L->tl, 0, 2 * kTlCount * sizeof(unsigned long long)), "memset");
+        } else if (!on && L->tl) {
+            ck(cudaDeviceSynchronize(), "sync");
+            ck(cudaFree(L->tl), "cudaFree");
+            L->tl = nullptr;
+        }
+    });
+}
+
+int perseus_layer_read_timeline(perseus_layer* L, uint64_t* start_end, int n) {
+    return guarded([&] {
+        if (!L->tl) throw sigsim::ConfigError("timeline is off");
+        std::vector<unsigned long long> h(2 * kTlCount);
+        ck(cudaMemcpy(h.data(), L->tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "memcpy");
+        for (int i = 0; i < n && i < kTlCount; ++i) {
+            start_end[2 * i] = h[2 * i] ? ~h[2 * i] : 0;
+            start_end[2 * i + 1] = h[2 * i + 1];
+        }
+    });
+}
+
+int perseus_layer_set_stage_timing(perseus_layer* L, int on) {
+    return guarded([&] { L->stage_timing = on != 0; });
+}
+
 int perseus_layer_read_timing(perseus_layer* L, float* ms, int n) {
     return guarded([&] {
+        if (!L->timed_last) throw sigsim::ConfigError("stage timing was off for the last forward");
         ck(cudaEventSynchronize(L->ev[5]), "event sync");
         for (int i = 0; i < n && i < 5; ++i) ck(cudaEventElapsedTime(&ms[i], L->ev[i], L->ev[i + 1]), "elapsed");
     });

@@ -3,6 +3,8 @@
 
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <utility>
 
 #include "perseus_internal.h"
 
@@ -34,6 +36,7 @@ struct DevCtx {
     int32_t* hist;       // [2][hist_blocks][E]: per-256-token-block expert histogram (parity halves)
     int32_t hist_blocks; // ceil(S/256)
     int32_t gate_splits; // tensor-core router: K splits, logits = sum of [gate_splits][S][E] partials
+    int32_t weights_late; // 1: the router ran on a side stream; the fused kernel's copy warps write weights
     const int32_t* zipf_ids;  // [S*k]: reference Zipf draws (routing == ZIPF)
     bf16* hbuf;          // [R_max][I]
 
@@ -65,8 +68,71 @@ struct DevCtx {
     uint32_t* sched;      // [4]: work-item / copy-unit counters
     int32_t* send_first;  // [E]: first send position of each expert's tiles
     int32_t* pairs;       // [max_recv][2]: M-tile pairs (recv positions, -1 = none) in processing order
+    int32_t self_head;    // minimum self pairs processed before the remote ones
+    float head_ratio;     // est. link time of one tile / compute time of one M-tile pair
 
     unsigned long long* stats;  // [kStatCount]
+    unsigned long long* fwd_t;  // [kFwdSlots]: this forward's communication timestamps (P > 1)
+    unsigned long long* tl;     // [2 * kTlCount] kernel timeline of the last forward (~start, end) or null
 };
+
+// kernel ids of the diagnostic timeline (DevCtx::tl)
+enum TlKernel : int { kTlGate = 0, kTlRoute, kTlPerm, kTlPlan, kTlFused, kTlCombine, kTlDispatch, kTlGemm1, kTlGemm2,
+                      kTlCount };
+
+#ifdef __CUDACC__
+// Launch with programmatic stream serialization (the kernel calls pdl_wait()
+// before touching anything an earlier kernel wrote).
+template <typename... Params, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+__device__ __forceinline__ uint64_t fwd_now() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Kernel timeline (diagnostics, perseus_layer_set_timeline): the first CTAs
+// record ~start (max of ~t = min of t), the last CTAs their end (globaltimer).
+__device__ __forceinline__ void tl_start(const DevCtx& c, int id) {
+    if (c.tl && threadIdx.x == 0 && blockIdx.x < 4) atomicMax(c.tl + 2 * id, ~fwd_now());
+}
+__device__ __forceinline__ void tl_end(const DevCtx& c, int id, bool me) {
+    if (c.tl && me && blockIdx.x + 4 >= gridDim.x) atomicMax(c.tl + 2 * id + 1, fwd_now());
+}
+
+// Routing weights of token t: softmax over its k chosen experts' logits (the
+// sum of the router's split-K partials in fixed order) -> weights[t][0..k).
+// One warp; lane j < k handles choice j.  (orc_route_weights)
+__device__ __forceinline__ void route_weights_warp(const DevCtx& c, int t, int lane) {
+    float mine = -INFINITY;
+    if (lane < c.k) {
+        const int e = c.ids[size_t(t) * c.k + lane];
+        mine = 0.f;
+        for (int q = 0; q < c.gate_splits; ++q) mine += c.logits[(size_t(q) * c.S + t) * c.E + e];
+    }
+    float m = mine;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float ex = lane < c.k ? expf(mine - m) : 0.f;
+    float s = ex;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane < c.k) c.weights[size_t(t) * c.k + lane] = ex / s;
+}
+#endif
 
 }  // namespace perseus

@@ -20,6 +20,8 @@
 // rows and discards them.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <cstring>
 
 #include <algorithm>
 
@@ -48,7 +50,8 @@ constexpr int kSelfWindow = 160;  // self tiles (x 512 KB at H=2048) copied ahea
 constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 
 struct Args {
-    int32_t n1, n2, kb1, kb2, lag, pad;
+    int32_t n1, n2, kb1, kb2, lag;
+    int32_t pf;  // L2 prefetch: distance in k-blocks (bits 0-7), operands (bit 8: A, bit 9: B)
     int64_t a1_row_base;
 };
 struct Item {
@@ -113,6 +116,7 @@ __device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, i
     };
     publish_member_warp(c, grp, c.cgroup_ctr + rt.cgroup, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
                         kStatCombineFences, kStatCombineSignals);
+    if (lane == 0) atomicMax(c.fwd_t + kFwdCombLast, fwd_now());
 }
 
 __device__ __forceinline__ uint32_t pk(const uint32_t* v, int i) {
@@ -137,10 +141,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     int32_t* ring = reinterpret_cast<int32_t*>(rempty + kRing);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ring + kRing);
 
-    const PlanHeader hdr = *c.hdr;  // identical in both CTAs: they return together
-    if (hdr.error) return;
-    const int T = hdr.n_pairs;
-    const int total = T * (f.n1 + f.n2);
     const int warp = warp_id(), lane = lane_id();
     const uint32_t crank = cluster_ctarank();
     const bool lead = crank == 0;
@@ -172,16 +172,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // everything above overlapped the previous kernel's tail (PDL); from here
+    // on the plan, heap and flags of this forward are read
+    pdl_wait();
+    tl_start(c, kTlFused);
+    PlanHeader hdr = *c.hdr;  // identical in both CTAs
+    if (hdr.error) hdr.n_pairs = hdr.n_send = hdr.n_send_remote = 0;  // no work; both CTAs fall through
+    const int T = hdr.n_pairs;
+    const int total = T * (f.n1 + f.n2);
     const uint64_t t_cta0 = globaltimer();
 
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- scheduler (leader) + TMA producer (both) ----------------
-            unsigned long long wait_d = 0, wait_g = 0;
+            // One item of lookahead: the next item is taken a few k-blocks before
+            // the current one ends (optionally, operand k-blocks are prefetched
+            // into L2 that many blocks ahead of their TMA load, f.pf).
+            unsigned long long wait_d = 0, wait_g = 0, wait_r = 0;
             int stage = 0, slot = 0;
             uint32_t phase = 0, rphase = 0;
             const uint32_t* dflags = c.dflag[c.rank] + size_t(c.par) * c.T_max;
-            while (true) {
+            auto grab = [&]() {
                 int w;
                 if (lead) {
                     w = int(atomicAdd(&c.sched[0], 1u));
@@ -197,48 +208,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                     mbar_arrive_cluster(mapa(smem_u32(&rempty[slot]), 0));
                 }
                 if (++slot == kRing) { slot = 0; rphase ^= 1; }
-                if (w < 0) break;
-                const Item it = item_of(w, T, f);
-                const int t0 = c.pairs[2 * it.t], t1 = c.pairs[2 * it.t + 1];
-                const int mine = (crank == 0 || t1 < 0) ? t0 : t1;
-                const RecvTile rt = c.recv[mine];
-                int32_t a_row, b_row, nkb;
+                return w;
+            };
+            struct Op {
                 const CUtensorMap* ta;
                 const CUtensorMap* tb;
-                const uint64_t tw0 = globaltimer();
+                int32_t a_row, b_row, nkb, kind, mine;
+            };
+            auto op_of = [&](int w) {
+                const Item it = item_of(w, T, f);
+                const int t0 = c.pairs[2 * it.t], t1 = c.pairs[2 * it.t + 1];
+                Op o;
+                o.mine = (crank == 0 || t1 < 0) ? t0 : t1;
+                const RecvTile rt = c.recv[o.mine];
+                o.kind = it.kind;
                 if (it.kind == 1) {
-                    const bool ok = rt.tile_id >= 0 ? wait_flag_geq(dflags + rt.tile_id, c.epoch, kWaitTimeoutNs)
-                                                    : wait_flag_geq(c.self_ready + mine, c.epoch, kWaitTimeoutNs);
-                    if (!ok) atomicAdd(&c.stats[kStatTimeouts], 1ull);
-                    wait_d += globaltimer() - tw0;
-                    a_row = int32_t(f.a1_row_base + rt.heap_row);
-                    b_row = rt.e_local * 2 * c.I + it.nb * 128 + (crank ? c.I : 0);  // gate | up
-                    nkb = f.kb1;
-                    ta = &tm_a1;
-                    tb = &tm_b1;
+                    o.a_row = int32_t(f.a1_row_base + rt.heap_row);
+                    o.b_row = rt.e_local * 2 * c.I + it.nb * 128 + (crank ? c.I : 0);  // gate | up
+                    o.nkb = f.kb1;
+                    o.ta = &tm_a1;
+                    o.tb = &tm_b1;
                 } else {
-                    if (!wait_flag_geq(c.g1_done + mine, uint32_t(f.n1), kWaitTimeoutNs))
+                    o.a_row = int32_t(rt.heap_row);
+                    o.b_row = rt.e_local * c.H + it.nb * 256 + int(crank) * 128;
+                    o.nkb = f.kb2;
+                    o.ta = &tm_a2;
+                    o.tb = &tm_b2;
+                }
+                return o;
+            };
+            const int pf_dist = f.pf & 0xff;
+            auto prefetch = [&](const Op& o, int kb) {
+                if (f.pf & 0x100) tma_prefetch_l2_2d(o.ta, kb * kBK, o.a_row);
+                if (f.pf & 0x200) tma_prefetch_l2_2d(o.tb, kb * kBK, o.b_row);
+            };
+            int w = grab();
+            Op cur{};
+            if (w >= 0) cur = op_of(w);
+            while (w >= 0) {
+                // dependencies of the current item
+                const uint64_t tw0 = globaltimer();
+                if (cur.kind == 1) {
+                    const int tile_id = c.recv[cur.mine].tile_id;
+                    const bool ok = tile_id >= 0 ? wait_flag_geq(dflags + tile_id, c.epoch, kWaitTimeoutNs)
+                                                 : wait_flag_geq(c.self_ready + cur.mine, c.epoch, kWaitTimeoutNs);
+                    if (!ok) atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                    const uint64_t dw = globaltimer() - tw0;
+                    wait_d += dw;
+                    if (tile_id >= 0) wait_r += dw;
+                } else {
+                    if (!wait_flag_geq(c.g1_done + cur.mine, uint32_t(f.n1), kWaitTimeoutNs))
                         atomicAdd(&c.stats[kStatTimeouts], 1ull);
                     wait_g += globaltimer() - tw0;
-                    a_row = int32_t(rt.heap_row);
-                    b_row = rt.e_local * c.H + it.nb * 256 + int(crank) * 128;
-                    nkb = f.kb2;
-                    ta = &tm_a2;
-                    tb = &tm_b2;
                 }
                 fence_proxy_async();
-                for (int kb = 0; kb < nkb; ++kb) {
+                int wn = -2;  // not taken yet
+                Op nxt{};
+                const int take_at = max(0, cur.nkb - max(pf_dist, 1));
+                for (int kb = 0; kb < cur.nkb; ++kb) {
+                    if (kb == take_at) {
+                        wn = grab();
+                        if (wn >= 0) nxt = op_of(wn);
+                    }
+                    if (pf_dist > 0) {
+                        const int pk = kb + pf_dist;
+                        if (pk < cur.nkb) prefetch(cur, pk);
+                        else if (wn >= 0 && pk - cur.nkb < nxt.nkb) prefetch(nxt, pk - cur.nkb);
+                    }
                     uint8_t* sa = smem + stage * kStage;
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (lead) mbar_arrive_expect_tx(&full[stage], 2 * kStage);
                     const uint32_t fb = mapa(smem_u32(&full[stage]), 0);
-                    tma_load_2d_pair(sa, ta, fb, kb * kBK, a_row);
-                    tma_load_2d_pair(sa + kA, tb, fb, kb * kBK, b_row);
+                    tma_load_2d_pair(sa, cur.ta, fb, kb * kBK, cur.a_row);
+                    tma_load_2d_pair(sa + kA, cur.tb, fb, kb * kBK, cur.b_row);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
+                if (wn == -2) {
+                    wn = grab();
+                    if (wn >= 0) nxt = op_of(wn);
+                }
+                w = wn;
+                cur = nxt;
             }
             atomicAdd(&c.stats[kStatWaitDispatchNs], wait_d);
             atomicAdd(&c.stats[kStatWaitG1Ns], wait_g);
+            atomicAdd(&c.stats[kStatWaitRemoteNs], wait_r);
         }
     } else if (warp == 1) {
         if (lane == 0 && lead) {
@@ -246,19 +300,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const uint32_t idesc = idesc_bf16_f32(2 * kBM, kBN);
             int stage = 0, slot = 0, acc = 0;
             uint32_t phase = 0, rphase = 0, aphase = 0;
+            // issue-side stall accounting (SM cycles): waiting for the next item,
+            // for a free accumulator (epilogue back-pressure), for operand stages
+            long long cy_ring = 0, cy_acc = 0, cy_data = 0;
+            const long long cy0 = clock64();
             while (true) {
+                long long t = clock64();
                 mbar_wait(&rfull[slot], rphase);
+                cy_ring += clock64() - t;
                 const int w = ring[slot];
                 mbar_arrive(&rempty[slot]);
                 if (++slot == kRing) { slot = 0; rphase ^= 1; }
                 if (w < 0) break;
                 const Item it = item_of(w, T, f);
                 const int nkb = it.kind == 1 ? f.kb1 : f.kb2;
+                t = clock64();
                 mbar_wait(&tempty[acc], aphase ^ 1);
+                cy_acc += clock64() - t;
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * kBN);
                 for (int kb = 0; kb < nkb; ++kb) {
+                    t = clock64();
                     mbar_wait(&full[stage], phase);
+                    cy_data += clock64() - t;
                     tc_fence_after();
                     uint8_t* sa = smem + stage * kStage;
                     const uint64_t adesc = smem_desc_sw128(sa);
@@ -272,6 +336,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 umma_commit_pair(&tfull[acc]);
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
+            atomicAdd(&c.stats[kStatMmaCycles], (unsigned long long)(clock64() - cy0));
+            atomicAdd(&c.stats[kStatMmaRingWait], (unsigned long long)cy_ring);
+            atomicAdd(&c.stats[kStatMmaAccWait], (unsigned long long)cy_acc);
+            atomicAdd(&c.stats[kStatMmaDataWait], (unsigned long long)cy_data);
         }
     } else if (warp < 4 || warp >= 8) {
         // ---------------- copy warps: dispatch puts ----------------
@@ -282,7 +350,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const int self_units = (hdr.n_send - hdr.n_send_remote) * kUnitsPerTile;
         const uint64_t tc0 = globaltimer();
         bool remote_q = warp >= 8;
-        bool other_done = false;
+        bool other_done = false, first_remote = true;
         while (true) {
             int u = 0;
             if (lane == 0) u = int(atomicAdd(&c.sched[remote_q ? 1 : 2], 1u));
@@ -315,6 +383,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const int r0 = (u % kUnitsPerTile) * kUnitRows;
             if (r0 >= st.rows) continue;
             const int nrows = min(kUnitRows, st.rows - r0);
+            if (remote_q && first_remote) {
+                if (lane == 0) atomicMin(c.fwd_t + kFwdDispFirst, fwd_now());
+                first_remote = false;
+            }
             copy_unit(c, st, r0, nrows, lane);
             __syncwarp();
             uint32_t done = 0;
@@ -335,8 +407,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             };
             publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
                                 kStatDispatchFences, kStatDispatchSignals);
+            if (lane == 0) atomicMax(c.fwd_t + kFwdDispLast, fwd_now());
         }
         if (lane == 0) atomicAdd(&c.stats[kStatCopyNs], (unsigned long long)(globaltimer() - tc0));
+        // the routing weights (router GEMM ran on a side stream), after the puts
+        if (c.weights_late) {
+            const int cw = warp < 4 ? warp - 2 : warp - 6;  // 0..5
+            for (int t = blockIdx.x * 6 + cw; t < c.S; t += gridDim.x * 6) route_weights_warp(c, t, lane);
+        }
     } else {
         // ---------------- epilogue (4 warps, this CTA's 128 accumulator rows) ----------------
         const int q = warp & 3;
@@ -344,6 +422,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         int acc = 0, slot = 0;
         uint32_t aphase = 0, rphase = 0;
         int pend_ti = -1, pend_nb = 0;
+        bool first_put = true;
         const uint32_t tempty_lead = mapa(smem_u32(&tempty[0]), 0);
         const uint32_t rempty_lead = mapa(smem_u32(&rempty[0]), 0);
         while (true) {
@@ -398,7 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             } else {
                 if (mine >= 0) {
                     bf16* dst = c.ybuf[rt.src] + (size_t(c.par) * c.Y_rows + size_t(rt.ybuf_row + row)) * c.H + it.nb * 256;
-                    if (rt.src == c.rank) {
+                    if (rt.src == c.rank && !(f.pf & 0x400)) {
 #pragma unroll 1
                         for (int cc = 0; cc < 256; cc += 32) {
                             uint32_t v32[32];
@@ -413,6 +492,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
                         for (int cc = 0; cc < 4; ++cc) bulk_commit();
                     } else {
+                        if (first_put) {
+                            if (lane == 0) atomicMin(c.fwd_t + kFwdCombFirst, fwd_now());
+                            first_put = false;
+                        }
                         uint8_t* srow_p = stage_out + (q * 32 + lane) * kStgRow;
                         const uint32_t srow = smem_u32(srow_p);
 #pragma unroll 1
@@ -458,11 +541,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             finish_tile(c, f.n2, pend_ti, pend_nb);
         }
     }
+    pdl_launch_dependents();  // the combine's launch overlaps this CTA's teardown
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
     if (threadIdx.x == 0) atomicAdd(&c.stats[kStatCtaNs], (unsigned long long)(globaltimer() - t_cta0));
+    tl_end(c, kTlFused, threadIdx.x == 0);
     if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+}
+
+// L2 prefetch of operand boxes ahead of their TMA loads; PERSEUS_PREFETCH="<dist>[,a][,b]"
+// overrides the default (experiments)
+static int prefetch_cfg() {
+    static int cfg = [] {
+        const char* e = getenv("PERSEUS_PREFETCH");
+        if (!e) return 0;
+        int dist = atoi(e), bits = 0;
+        if (strchr(e, 'a')) bits |= 0x100;
+        if (strchr(e, 'b')) bits |= 0x200;
+        if (strchr(e, 's')) bits |= 0x400;  // self GEMM2 tiles through the staged bulk-store path
+        return (dist & 0xff) | bits;
+    }();
+    return cfg;
 }
 
 cudaError_t configure_moe2() {
@@ -477,7 +577,7 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     f.kb1 = c.H / kBK;
     f.kb2 = c.I / kBK;
     f.lag = std::max(1, (grid + f.n1 - 1) / f.n1);  // pairs: half as many concurrent items
-    f.pad = 0;
+    f.pf = prefetch_cfg();
     f.a1_row_base = a1_row_base;
     DevCtx cc = c;
     void* args[] = {const_cast<CUtensorMap*>(&a1), const_cast<CUtensorMap*>(&b1), const_cast<CUtensorMap*>(&a2),
@@ -487,15 +587,17 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     cfg.blockDim = dim3(384);  // warps 2-3 and 8-11 copy, 4-7 epilogue
     cfg.dynamicSmemBytes = kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
-    attr[0].val.cooperative = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the plan kernel
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
-        cfg.numAttrs = 0;  // cooperative + clusters rejected: 1 CTA/SM, grid = #SMs keeps them co-resident
+        cfg.numAttrs = 1;  // cooperative + clusters rejected: 1 CTA/SM, grid = #SMs keeps them co-resident
         e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
     }
     return e;

@@ -104,7 +104,22 @@ enum StatSlot : int {
     kStatWaitG1Ns,        // ... blocked on GEMM1 -> GEMM2 tile dependencies
     kStatCopyNs,          // ... copy-warp busy time (dispatch puts)
     kStatCtaNs,           // ... summed CTA lifetimes
+    kStatWaitRemoteNs,    // ... producer time blocked on REMOTE dispatch flags only (exposed dispatch)
+    kStatDispatchSpanNs,  // first remote dispatch store -> last remote tile signalled, per forward
+    kStatCombineSpanNs,   // first remote combine store -> last remote combine tile signalled
+    kStatCombineWaitNs,   // longest combine-kernel CTA wait for its combine flags (exposed combine)
+    kStatMmaCycles,       // fused pair kernel, MMA issuer: SM cycles in the issue loop
+    kStatMmaRingWait,     // ... waiting for the next work item
+    kStatMmaAccWait,      // ... waiting for a free TMEM accumulator (epilogue back-pressure)
+    kStatMmaDataWait,     // ... waiting for operand stages (TMA)
     kStatCount
+};
+
+// Per-forward communication timestamps (globaltimer ns), reset by the plan
+// kernel and folded into the stats by the combine kernel's last CTA.
+enum FwdSlot : int {
+    kFwdDispFirst = 0, kFwdDispLast, kFwdCombFirst, kFwdCombLast, kFwdUnused, kFwdWaitMax, kFwdDoneCtas,
+    kFwdSlots = 8
 };
 
 constexpr uint64_t kWaitTimeoutNs = 4000000000ull;  // 4 s: a lost signal errors out, never hangs

@@ -1,4 +1,5 @@
-// plan.cu — the per-forward device plan, 4 warps, warp-level scans.
+// plan.cuh — the per-forward device plan, 4 warps, warp-level scans (run by
+// k_plan4, kernels.cu).
 //
 // Computes, from the [P][E] per-(src, expert) count table every rank
 // published, exactly the reference's dispatch layout (workload.cpp:132-213):
@@ -11,6 +12,7 @@
 // order, M-tile pairs).  The plan is latency-bound (a few thousand integers),
 // so it runs as 4 independent warps with shuffle scans and three CTA
 // barriers, instead of block-wide scans over 1024 threads.
+#pragma once
 #include <cuda_runtime.h>
 
 #include "layer_dev.h"
@@ -49,24 +51,15 @@ __device__ int32_t warp_scan(int32_t* a, int n) {
     return total;
 }
 
-// position of item `idx` of stream q in an idx-major interleave of streams
-// with lengths n[0..P) (streams listed in `order`, skipping `skip`)
-__device__ __forceinline__ int interleave_pos(const int32_t* n, int P, int skip, int q, int idx) {
-    int pos = 0;
-    for (int z = 0; z < P; ++z) {
-        if (z == skip) continue;
-        pos += min(n[z], idx) + ((z < q && n[z] > idx) ? 1 : 0);
-    }
-    return pos;
-}
-
 }  // namespace
 
-__global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
-    extern __shared__ int32_t sm[];
+// The plan, run by threads 0..127 of one CTA (named barrier 1; `sm` holds
+// plan_smem_bytes()).
+__device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     const int P = c.P, E = c.E, El = c.E_loc, r = c.rank;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int PE = P * E;
+    auto sync128 = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     int32_t* T = sm;            // [P][E] counts
     int32_t* tb = T + PE;       // tile-id base per (s, e), s-major
     int32_t* hr = tb + PE;      // heap-row scan, (d, s, j) order
@@ -79,19 +72,24 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
     __shared__ int32_t dst_first[kMaxPes], dst_n[kMaxPes], dst_group[kMaxPes], n_dgroups;
     __shared__ int32_t src_first[kMaxPes], src_n[kMaxPes], src_group[kMaxPes], n_cgroups_pe;
     __shared__ int32_t src_pfirst[kMaxPes], src_np[kMaxPes];
+    // rotated schedules: sender r streams destination r+1, r+2, ... in turn, so
+    // receiver r gets source r-1, r-2, ... one at a time (one group completes
+    // after another instead of all at the end)
+    __shared__ int32_t send_base[kMaxPes], recv_base[kMaxPes], recv_pbase[kMaxPes], s_head;
 
     if (tid == 0) s_err = 0;
     if (tid < P && !wait_flag_geq(c.count_flag[r] + tid, c.epoch, kWaitTimeoutNs)) {
         atomicAdd(&c.stats[kStatTimeouts], 1ull);
         s_err = 1;
     }
-    __syncthreads();
+    sync128();
     const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
     for (int i = tid; i < PE; i += 128) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
     if (tid == 0) {
         for (int q = 0; q < 4; ++q) c.sched[q] = 0;
+        for (int q = 0; q < kFwdSlots; ++q) c.fwd_t[q] = (q & 1) || q == kFwdDoneCtas ? 0ull : ~0ull;  // min / max
     }
-    __syncthreads();
+    sync128();
 
     // ---- phase B: four independent scans ----
     if (warp == 0) {
@@ -157,9 +155,30 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
                 src_np[s] = pl - pf;
             }
             n_cgroups_pe = g;
+            int sb = 0, rb = 0, pb = 0;
+            for (int i = 1; i < P; ++i) {
+                const int dd = (r + i) % P, ss = (r - i + P) % P;
+                send_base[dd] = sb;
+                sb += dst_n[dd];
+                recv_base[ss] = rb;
+                rb += src_n[ss];
+                recv_pbase[ss] = pb;
+                pb += src_np[ss];
+            }
+            // self pairs ahead of the remote ones: enough to cover the arrival of
+            // the first source's first signal group (host-estimated link time per
+            // tile / compute time per pair), at least ~two waves of GEMM1 items
+            const int n_self_p = src_np[r];
+            int head = n_self_p;
+            if (P > 1) {
+                const int fs = (r - 1 + P) % P;
+                const int fg = c.group_size > 0 ? min(c.group_size, src_n[fs]) : src_n[fs];
+                head = min(n_self_p, max(c.self_head, int(ceilf(float(fg) * c.head_ratio))));
+            }
+            s_head = head;
         }
     }
-    __syncthreads();
+    sync128();
 
     const int gs = c.group_size;
     const int32_t n_send = s_n_send, n_recv = s_n_recv, n_pairs = s_n_pairs, rows_in_r = s_rows_in;
@@ -199,7 +218,7 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
                 st.pad = 0;
                 c.send[p] = st;
                 c.send_done[p] = 0;
-                if (d != r) c.sorder[interleave_pos(dst_n, P, r, d, p - dst_first[d])] = p;
+                if (d != r) c.sorder[send_base[d] + (p - dst_first[d])] = p;
             }
         }
         for (int g = t2; g < n_groups; g += 64) {
@@ -241,13 +260,19 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
                 c.recv[p] = rt;
                 c.tile_ctr[p] = 0;
                 c.g1_done[p] = 0;
-                // processing order: self tiles first, then remote tiles idx-major over sources
-                c.rorder[s == r ? p : n_recv_self + interleave_pos(src_n, P, r, s, p - src_first[s])] = p;
+                // processing order (1-CTA kernel): self tiles first, then remote tiles
+                // source by source in arrival order
+                c.rorder[s == r ? p : n_recv_self + recv_base[s] + (p - src_first[s])] = p;
             }
             // M-tile pairs (consecutive chunks of one segment; odd tail paired with -1)
+            // in processing order: a head of self pairs (work while the first
+            // remote group is in flight), the remote pairs source by source in
+            // arrival order (their outputs travel back, so they finish early),
+            // then the rest of the self pairs — the tail needs no NVLink round trip
+            const int n_rem_p = n_pairs - src_np[r], head = s_head;
             for (int pi = 0; 2 * pi < nt; ++pi) {
                 const int q = pp[ks * El + j] + pi;
-                const int po = s == r ? q : src_np[r] + interleave_pos(src_np, P, r, s, q - src_pfirst[s]);
+                const int po = s == r ? (q < head ? q : q + n_rem_p) : head + recv_pbase[s] + (q - src_pfirst[s]);
                 if (po < c.max_recv) {
                     c.pairs[2 * po] = pos0 + 2 * pi;
                     c.pairs[2 * po + 1] = 2 * pi + 1 < nt ? pos0 + 2 * pi + 1 : -1;
@@ -267,7 +292,7 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
             c.cgroup_ctr[g] = 0;
         }
     }
-    __syncthreads();
+    sync128();
     if (tid == 0) {
         PlanHeader h;
         h.n_send = n_send;
@@ -286,12 +311,6 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
     }
 }
 
-size_t plan4_smem_bytes(const DevCtx& c) { return sizeof(int32_t) * (4 * size_t(c.P) * c.E + 4 * size_t(c.E) + 8); }
-
-cudaError_t configure_plan4(const DevCtx& c) {
-    return cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan4_smem_bytes(c)));
-}
-
-void launch_plan4(const DevCtx& c, cudaStream_t st) { k_plan4<<<1, 128, plan4_smem_bytes(c), st>>>(c); }
+inline size_t plan_smem_bytes(const DevCtx& c) { return sizeof(int32_t) * (4 * size_t(c.P) * c.E + 4 * size_t(c.E) + 8); }
 
 }  // namespace perseus

@@ -59,6 +59,12 @@ DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
 DEVI void tma_prefetch_desc(const void* desc) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
 }
+// L2 prefetch of one 2D box of a tensor map (no smem, no completion)
+DEVI void tma_prefetch_l2_2d(const void* desc, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(desc)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 // 2D tiled load global -> shared, completes `bytes` on `bar`.  c0 = inner (K)
 // coordinate in elements, c1 = row.
 DEVI void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1) {
@@ -259,6 +265,11 @@ DEVI uint32_t ld_acquire_sys(const uint32_t* p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+DEVI uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 DEVI uint32_t ld_relaxed_sys(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -269,6 +280,12 @@ DEVI uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// Programmatic dependent launch: the kernel's prologue may overlap the tail of
+// the previous kernel in the stream; pdl_wait() blocks until that kernel has
+// completed and its writes are visible (a no-op without the launch attribute).
+DEVI void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DEVI void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 DEVI uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

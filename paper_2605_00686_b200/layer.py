@@ -148,7 +148,28 @@ class MoELayer:
         check(lib.perseus_layer_read_count_table(self._h, t.ctypes.data_as(C.POINTER(C.c_int32))))
         return t
 
+    def set_stage_timing(self, on: bool = True) -> None:
+        """Record per-stage CUDA events in the following forwards (off by default)."""
+        check(lib.perseus_layer_set_stage_timing(self._h, int(bool(on))))
+
+    TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2")
+
+    def set_timeline(self, on: bool = True) -> None:
+        """Record a per-kernel device timeline of the following forwards (diagnostics)."""
+        check(lib.perseus_layer_set_timeline(self._h, int(bool(on))))
+
+    def timeline(self) -> dict:
+        """{kernel: (start_ns, end_ns)} of the last forward, relative to its first kernel start."""
+        n = len(self.TIMELINE_KERNELS)
+        buf = (C.c_uint64 * (2 * n))()
+        check(lib.perseus_layer_read_timeline(self._h, buf, n))
+        starts = [buf[2 * i] for i in range(n) if buf[2 * i]]
+        t0 = min(starts) if starts else 0
+        return {name: ((buf[2 * i] - t0), (buf[2 * i + 1] - t0) if buf[2 * i + 1] else None)
+                for i, name in enumerate(self.TIMELINE_KERNELS) if buf[2 * i]}
+
     def timing(self) -> List[float]:
+        """Stage times (ms) of the last forward; needs set_stage_timing(True)."""
         ms = (C.c_float * 5)()
         check(lib.perseus_layer_read_timing(self._h, ms, 5))
         return list(ms)
