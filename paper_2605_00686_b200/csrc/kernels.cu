@@ -209,7 +209,17 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     int32_t* hist_next = c.hist + size_t(c.par ^ 1) * c.hist_blocks * E;  // zeroed for the next forward
     for (int e = tid; e < E; e += kPermT) {
         int32_t before = 0, after = 0;
-        for (int q = 0; q < nb; ++q) {
+        int q = 0;
+        for (; q + 8 <= nb; q += 8) {  // 8 independent loads in flight (latency-bound kernel)
+            int32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = hist[size_t(q + u) * E + e];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (q + u < b) before += v[u]; else after += v[u];
+            }
+        }
+        for (; q < nb; ++q) {
             const int32_t v = hist[size_t(q) * E + e];
             if (q < b) before += v; else after += v;
         }
@@ -236,16 +246,21 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     if (b == 0 && tid == 0) c.offsets[E] = total;
     const int t = b * kPermT + tid;
     int32_t my[16];
-    if (t < c.S)
-        for (int j = 0; j < c.k; ++j) {
-            my[j] = c.ids[size_t(t) * c.k + j];
-            atomicOr(&bits[my[j] * (kPermT / 32) + (tid >> 5)], 1u << (tid & 31));
-        }
+    if (t < c.S) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < c.k) my[j] = c.ids[size_t(t) * c.k + j];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < c.k) atomicOr(&bits[my[j] * (kPermT / 32) + (tid >> 5)], 1u << (tid & 31));
+    }
     __syncthreads();
     if (t >= c.S) return;
     const int w = tid >> 5;
     const uint32_t below = (1u << (tid & 31)) - 1u;
-    for (int j = 0; j < c.k; ++j) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j >= c.k) break;
         const uint32_t* row = bits + my[j] * (kPermT / 32);
         int32_t rank = __popc(row[w] & below);
         for (int q = 0; q < w; ++q) rank += __popc(row[q]);
