@@ -30,6 +30,7 @@ void launch_dispatch(const DevCtx& c, cudaStream_t st);
 cudaError_t configure_moe();
 cudaError_t configure_moe2();
 cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
+                        const CUtensorMap* smaps,
                         const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
 cudaError_t launch_moe(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
                        const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
@@ -138,6 +139,7 @@ struct perseus_layer {
     bool connected = false;
 
     CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{}, tm_wg{}, tm_x{}, tm_xg{};
+    CUtensorMap* smaps = nullptr;  // device copy of the epilogue's TMA store maps (store_maps())
     const void* tm_x_ptr = nullptr;
     cudaEvent_t ev[6] = {};
     const void* last_x = nullptr;
@@ -217,7 +219,7 @@ void free_layer(perseus_layer* L) {
     void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
-                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl,
+                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl, L->smaps,
                     L->send_first, L->pairs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -228,6 +230,22 @@ void free_layer(perseus_layer* L) {
     if (L->ev_x) cudaEventDestroy(L->ev_x);
     if (L->ev_gate) cudaEventDestroy(L->ev_gate);
     delete L;
+}
+
+// TMA store maps of the pair kernel's epilogue (box 64 x 32, SW128), built once
+// the peers are mapped: [0] hbuf, [1 + p] PE p's combine buffer (both halves)
+const CUtensorMap* store_maps(perseus_layer* L) {
+    if (!L->smaps) {
+        std::vector<CUtensorMap> m(1 + kMaxPes);
+        m[0] = make_tmap(L->hbuf, uint64_t(L->R_max), uint64_t(L->I), 32);
+        for (int p = 0; p < L->world; ++p)
+            m[1 + p] = make_tmap(L->peer[p] + L->off_ybuf, 2 * uint64_t(L->Y_rows), uint64_t(L->H), 32);
+        void* d = nullptr;
+        ck(cudaMalloc(&d, m.size() * sizeof(CUtensorMap)), "cudaMalloc store maps");
+        ck(cudaMemcpy(d, m.data(), m.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "memcpy store maps");
+        L->smaps = static_cast<CUtensorMap*>(d);
+    }
+    return L->smaps;
 }
 
 void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream_t st) {
@@ -282,7 +300,8 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         if (side_gate) ck(cudaStreamWaitEvent(st, L->ev_gate, 0), "wait");  // router done before the persistent kernel
         if (tev) ck(cudaEventRecord(L->ev[2], st), "event");
         if (L->pair)
-            ck(launch_moe2(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),
+            ck(launch_moe2(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, store_maps(L), c, int64_t(c.par) * L->R_max,
+                           L->num_sms, st),
                "launch k_moe2");
         else
             ck(launch_moe(L->tm_a1, L->tm_b1, L->tm_a2, L->tm_b2, c, int64_t(c.par) * L->R_max, L->num_sms, st),

@@ -41,8 +41,10 @@ constexpr int kA = kBM * kBK * 2;         // 16 KB: this CTA's A rows
 constexpr int kBh = 128 * kBK * 2;        // 16 KB: this CTA's half of B
 constexpr int kStage = kA + kBh;          // 32 KB
 constexpr int kTmemCols = 512;
-constexpr int kStgRow = 128 + 16;
-constexpr int kStgBytes = 128 * kStgRow;
+constexpr int kStgRow = 128 + 16;              // partial-tile fallback: padded 128-byte rows
+constexpr int kStgWarp = 2 * 32 * 128;          // per epilogue warp: 2 x (32 rows x 64 cols bf16), SW128
+constexpr int kStgBytes = 4 * kStgWarp;         // (>= 128 * kStgRow)
+static_assert(kStgBytes >= 128 * kStgRow, "staging");
 constexpr int kRing = 8;
 constexpr int kUnitRows = 2;  // fine units: few tiles in flight, so tiles land one after another at link rate
 constexpr int kUnitsPerTile = kTileRows / kUnitRows;
@@ -52,6 +54,7 @@ constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 struct Args {
     int32_t n1, n2, kb1, kb2, lag;
     int32_t pf;  // L2 prefetch: distance in k-blocks (bits 0-7), operands (bit 8: A, bit 9: B)
+    const CUtensorMap* smaps;  // store maps, box 64 x 32, SW128: [0] hbuf, [1 + p] ybuf of PE p
     int64_t a1_row_base;
 };
 struct Item {
@@ -92,6 +95,27 @@ __device__ __forceinline__ void copy_unit(const DevCtx& c, const SendTile& st, i
         }
         for (; v < nvec; v += 32) dst[v] = __ldg(src + v);
     }
+}
+
+// One 32-row x 64-column bf16 chunk of an epilogue warp through its
+// double-buffered, 128B-swizzled staging slot into a TMA tensor store (lane 0
+// issues; one bulk group per chunk).  w[0..31] = 64 bf16 packed in pairs.
+__device__ __forceinline__ void store_chunk(uint8_t* stg_warp, int& buf, const uint32_t* w, int lane,
+                                            const CUtensorMap* map, int32_t col, int32_t row) {
+    uint8_t* b = stg_warp + buf * (32 * 128);
+    if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+    __syncwarp();
+    const uint32_t base = smem_u32(b) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        st_shared_v4(base + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(map, b, col, row);
+        bulk_commit();
+    }
+    buf ^= 1;
 }
 
 // combine-direction completion of one n-block of a remote M-tile (4 epilogue warps)
@@ -423,6 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         uint32_t aphase = 0, rphase = 0;
         int pend_ti = -1, pend_nb = 0;
         bool first_put = true;
+        uint8_t* stg_warp = stage_out + q * kStgWarp;
+        int sbuf = 0;
         const uint32_t tempty_lead = mapa(smem_u32(&tempty[0]), 0);
         const uint32_t rempty_lead = mapa(smem_u32(&rempty[0]), 0);
         while (true) {
@@ -444,8 +470,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             RecvTile rt;
             if (mine >= 0) rt = c.recv[mine];
             const bool valid = mine >= 0 && row < rt.rows;
+            const bool full_tile = mine >= 0 && rt.rows == kTileRows && !(f.pf & 0x400);
             if (it.kind == 1) {
-                if (mine >= 0) {
+                if (full_tile) {
+                    // h = silu(gate) * up -> hbuf via TMA tensor stores
+#pragma unroll 1
+                    for (int cc = 0; cc < 128; cc += 64) {
+                        uint32_t o[32];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t gv[32], uv[32];
+                            tmem_ld_32x32b_x32(taddr + cc + 32 * h, gv);
+                            tmem_ld_32x32b_x32(taddr + 128 + cc + 32 * h, uv);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                o[16 * h + i] = pack_bf16(silu_mul(__uint_as_float(gv[2 * i]), __uint_as_float(uv[2 * i])),
+                                                          silu_mul(__uint_as_float(gv[2 * i + 1]), __uint_as_float(uv[2 * i + 1])));
+                        }
+                        store_chunk(stg_warp, sbuf, o, lane, f.smaps, it.nb * 128 + cc, int32_t(rt.heap_row) + q * 32);
+                    }
+                } else if (mine >= 0) {
                     bf16* dst = c.hbuf + size_t(rt.heap_row + row) * c.I + it.nb * 128;
 #pragma unroll 1
                     for (int cc = 0; cc < 128; cc += 32) {
@@ -471,50 +516,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                     else mbar_arrive_cluster(tempty_lead + 8u * acc);
                 }
                 if (mine >= 0) {
+                    if (full_tile && lane == 0) {
+                        bulk_wait0();  // h rows written before GEMM2's TMA loads may read them
+                        fence_proxy_async();
+                    }
                     named_bar_sync(2, 128);
                     if (threadIdx.x == 128) atom_add_acq_rel_gpu(c.g1_done + mine, 1u);
                 }
             } else {
-                if (mine >= 0) {
+                if (full_tile) {
+                    // y tile -> the token owner's combine buffer (local or NVLink peer) via TMA tensor stores
+                    if (rt.src != c.rank && first_put) {
+                        if (lane == 0) atomicMin(c.fwd_t + kFwdCombFirst, fwd_now());
+                        first_put = false;
+                    }
+                    const CUtensorMap* ym = f.smaps + 1 + rt.src;
+                    const int32_t yrow = int32_t(size_t(c.par) * c.Y_rows + rt.ybuf_row) + q * 32;
+#pragma unroll 1
+                    for (int cc = 0; cc < 256; cc += 64) {
+                        uint32_t v0[32], v1[32], o[32];
+                        tmem_ld_32x32b_x32(taddr + cc, v0);
+                        tmem_ld_32x32b_x32(taddr + cc + 32, v1);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            o[i] = pk(v0, 2 * i);
+                            o[16 + i] = pk(v1, 2 * i);
+                        }
+                        store_chunk(stg_warp, sbuf, o, lane, ym, it.nb * 256 + cc, yrow);
+                    }
+                    if (lane != 0) {
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) bulk_commit();  // keep per-lane group counts uniform
+                    }
+                } else if (mine >= 0) {
+                    // partial tile: direct 16-byte stores of the valid rows (local or peer)
                     bf16* dst = c.ybuf[rt.src] + (size_t(c.par) * c.Y_rows + size_t(rt.ybuf_row + row)) * c.H + it.nb * 256;
-                    if (rt.src == c.rank && !(f.pf & 0x400)) {
 #pragma unroll 1
-                        for (int cc = 0; cc < 256; cc += 32) {
-                            uint32_t v32[32];
-                            tmem_ld_32x32b_x32(taddr + cc, v32);
-                            tmem_ld_wait();
-                            if (valid) {
+                    for (int cc = 0; cc < 256; cc += 32) {
+                        uint32_t v32[32];
+                        tmem_ld_32x32b_x32(taddr + cc, v32);
+                        tmem_ld_wait();
+                        if (valid) {
 #pragma unroll
-                                for (int v = 0; v < 4; ++v)
-                                    st_global_v4(dst + cc + v * 8, pk(v32, 8 * v), pk(v32, 8 * v + 2), pk(v32, 8 * v + 4), pk(v32, 8 * v + 6));
-                            }
-                        }
-#pragma unroll
-                        for (int cc = 0; cc < 4; ++cc) bulk_commit();
-                    } else {
-                        if (first_put) {
-                            if (lane == 0) atomicMin(c.fwd_t + kFwdCombFirst, fwd_now());
-                            first_put = false;
-                        }
-                        uint8_t* srow_p = stage_out + (q * 32 + lane) * kStgRow;
-                        const uint32_t srow = smem_u32(srow_p);
-#pragma unroll 1
-                        for (int cc = 0; cc < 256; cc += 64) {
-                            uint32_t v0[32], v1[32];
-                            tmem_ld_32x32b_x32(taddr + cc, v0);
-                            tmem_ld_32x32b_x32(taddr + cc + 32, v1);
-                            tmem_ld_wait();
-                            bulk_wait_read0();
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                st_shared_v4(srow + v * 16, pk(v0, 8 * v), pk(v0, 8 * v + 2), pk(v0, 8 * v + 4), pk(v0, 8 * v + 6));
-                                st_shared_v4(srow + 64 + v * 16, pk(v1, 8 * v), pk(v1, 8 * v + 2), pk(v1, 8 * v + 4), pk(v1, 8 * v + 6));
-                            }
-                            fence_proxy_async_smem();
-                            if (valid) bulk_store(dst + cc, srow_p, 128);
-                            bulk_commit();
+                            for (int v = 0; v < 4; ++v)
+                                st_global_v4(dst + cc + v * 8, pk(v32, 8 * v), pk(v32, 8 * v + 2), pk(v32, 8 * v + 4), pk(v32, 8 * v + 6));
                         }
                     }
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) bulk_commit();
                 } else {
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) bulk_commit();
@@ -559,7 +609,7 @@ static int prefetch_cfg() {
         int dist = atoi(e), bits = 0;
         if (strchr(e, 'a')) bits |= 0x100;
         if (strchr(e, 'b')) bits |= 0x200;
-        if (strchr(e, 's')) bits |= 0x400;  // self GEMM2 tiles through the staged bulk-store path
+        if (strchr(e, 'd')) bits |= 0x400;  // epilogue: direct stores instead of TMA tensor stores
         return (dist & 0xff) | bits;
     }();
     return cfg;
@@ -570,7 +620,7 @@ cudaError_t configure_moe2() {
 }
 
 cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
-                        const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st) {
+                        const CUtensorMap* smaps, const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st) {
     Args f;
     f.n1 = c.I / 128;
     f.n2 = c.H / 256;
@@ -578,6 +628,7 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     f.kb2 = c.I / kBK;
     f.lag = std::max(1, (grid + f.n1 - 1) / f.n1);  // pairs: half as many concurrent items
     f.pf = prefetch_cfg();
+    f.smaps = smaps;
     f.a1_row_base = a1_row_base;
     DevCtx cc = c;
     void* args[] = {const_cast<CUtensorMap*>(&a1), const_cast<CUtensorMap*>(&b1), const_cast<CUtensorMap*>(&a2),
