@@ -165,6 +165,16 @@ int perseus_layer_forward(perseus_layer* layer, const void* x, void* out, void* 
 int perseus_layer_forward_host(perseus_layer* layer, const void* x_host, void* out_host,
                                void* stream);
 
+/* Pipelined end-to-end forward for a stream of batches (serving): enqueues the
+ * H2D copy of x_host on an upload stream, the forward on the layer's stream and
+ * the D2H copy into out_host on a download stream, and returns without waiting,
+ * so batch n+1's upload and batch n-1's download overlap batch n's forward (two
+ * device staging slots).  Host buffers should be pinned and must stay valid
+ * until perseus_layer_host_wait(). */
+int perseus_layer_forward_host_async(perseus_layer* layer, const void* x_host, void* out_host);
+/* Wait until every enqueued forward_host_async has its output in host memory. */
+int perseus_layer_host_wait(perseus_layer* layer);
+
 /* Phased forward for P ranks emulated on one device: phase p of every rank
  * must complete before phase p+1 of any rank (no cross-launch spin-waits on
  * one GPU).  PERSEUS_PHASE_ALL == perseus_layer_forward. */

@@ -86,6 +86,8 @@ def _load():
         "perseus_fill_synthetic_x": (C.c_int, [vp, vp, u64, vp]),
         "perseus_layer_forward": (C.c_int, [vp, vp, vp, vp]),
         "perseus_layer_forward_host": (C.c_int, [vp, vp, vp, vp]),
+        "perseus_layer_forward_host_async": (C.c_int, [vp, vp, vp]),
+        "perseus_layer_host_wait": (C.c_int, [vp]),
         "perseus_layer_forward_phase": (C.c_int, [vp, C.c_int, vp, vp, vp]),
         "perseus_layer_counters": (C.c_int, [vp, P(Counters)]),
         "perseus_layer_read_routing": (C.c_int, [vp, P(i32), P(C.c_float), P(i32), P(i32)]),

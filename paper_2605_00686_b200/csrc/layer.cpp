@@ -110,6 +110,12 @@ struct perseus_layer {
 
     // local
     bf16 *x_stage = nullptr, *out_stage = nullptr;
+    // pipelined host API (perseus_layer_forward_host_async): 2 staging slots,
+    // upload / download streams and per-slot events
+    bf16 *xs2[2] = {nullptr, nullptr}, *os2[2] = {nullptr, nullptr};
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_fwd[2] = {nullptr, nullptr}, ev_down[2] = {nullptr, nullptr};
+    uint64_t host_calls = 0;
     bf16 *wg = nullptr, *w1 = nullptr, *w2 = nullptr, *hbuf = nullptr;
     float *logits = nullptr, *weights = nullptr;
     int32_t *ids = nullptr, *counts = nullptr, *offsets = nullptr, *rows = nullptr, *pos = nullptr,
@@ -141,6 +147,8 @@ struct perseus_layer {
     CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{}, tm_wg{}, tm_x{}, tm_xg{};
     CUtensorMap* smaps = nullptr;  // device copy of the epilogue's TMA store maps (store_maps())
     const void* tm_x_ptr = nullptr;
+    CUtensorMap tm_x_c[2]{}, tm_xg_c[2]{};  // second-level cache: the two pipelined staging slots
+    const void* tm_x_cptr[2] = {nullptr, nullptr};
     cudaEvent_t ev[6] = {};
     const void* last_x = nullptr;
 
@@ -227,6 +235,14 @@ void free_layer(perseus_layer* L) {
         if (e) cudaEventDestroy(e);
     if (L->stream) cudaStreamDestroy(L->stream);
     if (L->stream2) cudaStreamDestroy(L->stream2);
+    for (int i = 0; i < 2; ++i) {
+        if (L->xs2[i]) cudaFree(L->xs2[i]);
+        if (L->os2[i]) cudaFree(L->os2[i]);
+        for (cudaEvent_t e : {L->ev_up[i], L->ev_fwd[i], L->ev_down[i]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (L->up) cudaStreamDestroy(L->up);
+    if (L->down) cudaStreamDestroy(L->down);
     if (L->ev_x) cudaEventDestroy(L->ev_x);
     if (L->ev_gate) cudaEventDestroy(L->ev_gate);
     delete L;
@@ -255,8 +271,17 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     if (x) L->last_x = x;
     DevCtx c = L->ctx(x ? x : L->last_x, out);
     if (c.x != L->tm_x_ptr) {  // TMA maps over the caller's token buffer (router tiles + row gathers)
-        L->tm_x = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H));
-        L->tm_xg = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H), 1);
+        int hit = -1;
+        for (int i = 0; i < 2; ++i)
+            if (L->tm_x_cptr[i] == c.x) hit = i;
+        if (hit < 0) {
+            hit = (L->tm_x_cptr[0] == L->tm_x_ptr) ? 1 : 0;  // keep the other slot
+            L->tm_x_c[hit] = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H));
+            L->tm_xg_c[hit] = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H), 1);
+            L->tm_x_cptr[hit] = c.x;
+        }
+        L->tm_x = L->tm_x_c[hit];
+        L->tm_xg = L->tm_xg_c[hit];
         L->tm_x_ptr = c.x;
     }
     const bool all = phase == PERSEUS_PHASE_ALL;
@@ -547,6 +572,47 @@ int perseus_layer_forward_host(perseus_layer* L, const void* x_host, void* out_h
         run_phase(L, PERSEUS_PHASE_ALL, L->x_stage, L->out_stage, st);
         ck(cudaMemcpyAsync(out_host, L->out_stage, bytes, cudaMemcpyDeviceToHost, st), "D2H out");
         ck(cudaStreamSynchronize(st), "forward_host sync");
+    });
+}
+
+int perseus_layer_forward_host_async(perseus_layer* L, const void* x_host, void* out_host) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        const size_t bytes = size_t(L->S) * L->H * 2;
+        if (!L->up) {
+            ck(cudaStreamCreateWithFlags(&L->up, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&L->down, cudaStreamNonBlocking), "stream");
+            for (int i = 0; i < 2; ++i) {
+                ck(cudaMalloc(&L->xs2[i], bytes), "cudaMalloc");
+                ck(cudaMalloc(&L->os2[i], bytes), "cudaMalloc");
+                for (cudaEvent_t* e : {&L->ev_up[i], &L->ev_fwd[i], &L->ev_down[i]}) {
+                    ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+                    ck(cudaEventRecord(*e, L->stream), "event");
+                }
+            }
+        }
+        const int s = int(L->host_calls++ & 1);
+        // upload: after the forward that last read this slot
+        ck(cudaStreamWaitEvent(L->up, L->ev_fwd[s], 0), "wait");
+        ck(cudaMemcpyAsync(L->xs2[s], x_host, bytes, cudaMemcpyHostToDevice, L->up), "H2D x");
+        ck(cudaEventRecord(L->ev_up[s], L->up), "event");
+        // forward: after the upload and after the download that last read this slot's output
+        ck(cudaStreamWaitEvent(L->stream, L->ev_up[s], 0), "wait");
+        ck(cudaStreamWaitEvent(L->stream, L->ev_down[s], 0), "wait");
+        run_phase(L, PERSEUS_PHASE_ALL, L->xs2[s], L->os2[s], L->stream);
+        ck(cudaEventRecord(L->ev_fwd[s], L->stream), "event");
+        // download
+        ck(cudaStreamWaitEvent(L->down, L->ev_fwd[s], 0), "wait");
+        ck(cudaMemcpyAsync(out_host, L->os2[s], bytes, cudaMemcpyDeviceToHost, L->down), "D2H out");
+        ck(cudaEventRecord(L->ev_down[s], L->down), "event");
+    });
+}
+
+int perseus_layer_host_wait(perseus_layer* L) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        if (L->down) ck(cudaStreamSynchronize(L->down), "host_wait");
+        ck(cudaStreamSynchronize(L->stream), "host_wait");
     });
 }
 

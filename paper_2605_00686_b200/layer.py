@@ -110,6 +110,18 @@ class MoELayer:
                                              None if stream is None else _stream(stream)))
         return out_host
 
+    def forward_host_async(self, x_host: np.ndarray, out_host: np.ndarray) -> None:
+        """Pipelined end-to-end entry (serving a stream of batches): enqueue
+        H2D(x_host) -> forward -> D2H(out_host) and return; batch n+1's upload and
+        n-1's download overlap batch n's forward.  Both arrays must be uint16
+        [S, H], should be pinned, and must stay alive until host_wait()."""
+        assert x_host.dtype == np.uint16 and out_host.dtype == np.uint16
+        assert x_host.flags.c_contiguous and out_host.flags.c_contiguous
+        check(lib.perseus_layer_forward_host_async(self._h, x_host.ctypes.data, out_host.ctypes.data))
+
+    def host_wait(self) -> None:
+        check(lib.perseus_layer_host_wait(self._h))
+
     # ------------------------------------------------------------- evidence --
     def counters(self) -> Dict[str, int]:
         c = _lib.Counters()

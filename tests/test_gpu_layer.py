@@ -209,3 +209,29 @@ def test_other_baseline_shapes_single_gpu(oracle, preset, S, routing):
     subset = np.sort(np.random.default_rng(1).choice(S, 24, replace=False))
     _check_rank(oracle, pb, shape_of(m, S, 1), l, x, out, routing, 4, 0.0, 0, subset=subset)
     l.close()
+
+
+@pytest.mark.gpu
+def test_forward_host_async_pipeline_matches_blocking(oracle):
+    """perseus_layer_forward_host_async: several batches in flight (two staging
+    slots, upload/download streams) give exactly the blocking API's outputs."""
+    import torch
+    from tests.gpu_util import bf16_bits
+    pb = _pb()
+    m = _model(pb, **TINY)
+    l = pb.MoELayer(m, 256, routing="gate", seed=5)
+    xs, want = [], []
+    for seed in range(4):
+        x = torch.empty(256, 256, dtype=torch.bfloat16, device="cuda")
+        l.fill_synthetic_x(x, 11 + seed)
+        torch.cuda.synchronize()
+        xb = np.ascontiguousarray(bf16_bits(x))
+        xs.append(xb)
+        want.append(l.forward_host(xb))
+    outs = [np.zeros_like(xb) for xb in xs]
+    for i in range(4):
+        l.forward_host_async(xs[i], outs[i])
+    l.host_wait()
+    for i in range(4):
+        assert np.array_equal(outs[i], want[i]), i
+    l.close()
