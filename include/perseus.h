@@ -239,6 +239,62 @@ int perseus_layer_read_count_table(perseus_layer* layer, int32_t* table);
 int perseus_layer_set_timeline(perseus_layer* layer, int on);
 int perseus_layer_read_timeline(perseus_layer* layer, uint64_t* start_end, int n_kernels);
 
+/* ---- device event log (trace mode) -> the reference's RunTrace ----------
+ * With tracing on, every forward records what the kernels actually did:
+ * sender-side puts, fences and flag writes, and receiver-side observations of
+ * each remote tile's signal, with a content check of the tile at first
+ * observation (receive buffers are poisoned before the forward; a signal seen
+ * before the data landed is an ordering violation).  Events of one forward,
+ * all PEs concatenated, are turned into a sigsim::RunTrace by
+ * perseus_trace_analyze, which runs the reference's fence_accounting,
+ * verify_ordering and conservation_check on it (metrics.cpp:10-59,118-190). */
+enum {
+    PERSEUS_EV_DISPATCH_PUT = 1,    /* sender: a remote transfer tile's stores issued */
+    PERSEUS_EV_DISPATCH_FENCE = 2,  /* sender: a group's sys-scope fence */
+    PERSEUS_EV_DISPATCH_SIGNAL = 3, /* sender: one flag word written */
+    PERSEUS_EV_DISPATCH_SEEN = 4,   /* receiver: first observation of a tile's flag (+ content check) */
+    PERSEUS_EV_COMBINE_PUT = 5,
+    PERSEUS_EV_COMBINE_FENCE = 6,
+    PERSEUS_EV_COMBINE_SIGNAL = 7,
+    PERSEUS_EV_COMBINE_SEEN = 8
+};
+typedef struct perseus_trace_event {
+    uint64_t t;      /* globaltimer ns of the recording PE */
+    int32_t kind;    /* PERSEUS_EV_* */
+    int32_t pe;      /* recording PE */
+    int32_t peer;    /* sender events: destination PE; receiver events: source PE */
+    int32_t tile;    /* reference tile id (= flag id); -1 for fences */
+    int32_t group;   /* sender's signal group (-1: none) */
+    uint32_t bytes;  /* puts: payload bytes; SEEN: ns from signal seen to content complete */
+    uint32_t aux;    /* SIGNAL: 1 = first flag after its group's fence; SEEN: 1 = content complete when seen */
+    uint32_t pad;
+} perseus_trace_event;
+
+/* Turn tracing on/off (allocates the event log; poisons receive buffers per forward). */
+int perseus_layer_set_trace(perseus_layer* layer, int on);
+/* Events of the last forward (call with events = NULL to size). */
+int perseus_layer_read_trace(perseus_layer* layer, perseus_trace_event* events, size_t cap, size_t* n);
+
+typedef struct perseus_trace_report {
+    int64_t records;                   /* RunTrace records built */
+    int64_t fence_count[2];            /* fence_accounting per direction [dispatch, combine], all PEs */
+    int64_t flagged_signal_count[2];
+    int64_t ordering_violations[2];    /* verify_ordering: signal visible before the data landed */
+    int64_t late_tiles[2];             /* tiles whose content was incomplete when first seen */
+    int32_t conservation_ok[2];        /* conservation_check against the realised transfer list */
+    int64_t put_bytes[2];
+    char conservation_error[256];
+} perseus_trace_report;
+
+/* Build one sigsim::RunTrace per direction from the events of one forward (all
+ * PEs) and run the reference's checks.  `nic_ordering`: the protocol orders
+ * with flagged signals (NicFence: combined / nic_ordering) instead of fence
+ * markers (ProxyFence: vanilla / decoupled).  `transfers` = the dispatch
+ * transfers the PEs realised (perseus_layer_read_layout of every PE); the
+ * combine direction mirrors them (same tiles, reversed). */
+int perseus_trace_analyze(const perseus_trace_event* events, size_t n, int nic_ordering,
+                          const perseus_transfer* transfers, size_t n_transfers, perseus_trace_report* out);
+
 /* Record per-stage CUDA events in every following forward (off by default: each
  * event record costs stream time). */
 int perseus_layer_set_stage_timing(perseus_layer* layer, int on);

@@ -38,6 +38,32 @@ class Transfer(C.Structure):
                 ("bytes", C.c_uint64), ("tile_id", C.c_int64), ("heap_offset", C.c_uint64)]
 
 
+class TraceEvent(C.Structure):
+    _fields_ = [("t", C.c_uint64), ("kind", C.c_int32), ("pe", C.c_int32), ("peer", C.c_int32),
+                ("tile", C.c_int32), ("group", C.c_int32), ("bytes", C.c_uint32), ("aux", C.c_uint32),
+                ("pad", C.c_uint32)]
+
+
+EV_DISPATCH_PUT, EV_DISPATCH_FENCE, EV_DISPATCH_SIGNAL, EV_DISPATCH_SEEN = 1, 2, 3, 4
+EV_COMBINE_PUT, EV_COMBINE_FENCE, EV_COMBINE_SIGNAL, EV_COMBINE_SEEN = 5, 6, 7, 8
+
+
+class TraceReport(C.Structure):
+    _fields_ = [("records", C.c_int64), ("fence_count", C.c_int64 * 2), ("flagged_signal_count", C.c_int64 * 2),
+                ("ordering_violations", C.c_int64 * 2), ("late_tiles", C.c_int64 * 2),
+                ("conservation_ok", C.c_int32 * 2), ("put_bytes", C.c_int64 * 2),
+                ("conservation_error", C.c_char * 256)]
+
+    def as_dict(self):
+        d = {"records": self.records}
+        for i, direction in enumerate(("dispatch", "combine")):
+            d[direction] = {"fence_count": self.fence_count[i], "flagged_signal_count": self.flagged_signal_count[i],
+                            "ordering_violations": self.ordering_violations[i], "late_tiles": self.late_tiles[i],
+                            "conservation_ok": bool(self.conservation_ok[i]), "put_bytes": self.put_bytes[i]}
+        d["conservation_error"] = self.conservation_error.decode()
+        return d
+
+
 class LayerConfig(C.Structure):
     _fields_ = [("hidden_dim", C.c_int64), ("intermediate_dim", C.c_int64),
                 ("experts", C.c_int64), ("top_k", C.c_int64), ("tokens_per_pe", C.c_uint64),
@@ -96,6 +122,9 @@ def _load():
         "perseus_layer_read_timing": (C.c_int, [vp, P(C.c_float), C.c_int]),
         "perseus_layer_set_stage_timing": (C.c_int, [vp, C.c_int]),
         "perseus_layer_set_timeline": (C.c_int, [vp, C.c_int]),
+        "perseus_layer_set_trace": (C.c_int, [vp, C.c_int]),
+        "perseus_layer_read_trace": (C.c_int, [vp, P(TraceEvent), sz, P(sz)]),
+        "perseus_trace_analyze": (C.c_int, [P(TraceEvent), sz, C.c_int, P(Transfer), sz, P(TraceReport)]),
         "perseus_layer_read_timeline": (C.c_int, [vp, P(C.c_uint64), C.c_int]),
     }
     for name, (res, args) in sig.items():

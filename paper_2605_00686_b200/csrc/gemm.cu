@@ -107,6 +107,7 @@ __device__ __forceinline__ void finish_tile(const DevCtx& c, const GemmArgs& g, 
     if (lane == 0) {
         atomicAdd(&c.stats[kStatCombinePuts], 1ull);
         atomicAdd(&c.stats[kStatCombineBytes], (unsigned long long)rt.rows * c.H * 2);
+        if (c.trace) trace_ev(c, PERSEUS_EV_COMBINE_PUT, rt.src, rt.tile_id, rt.cgroup, uint32_t(rt.rows) * c.H * 2, 0, fwd_now());
     }
     const Group grp = c.cgroups[rt.cgroup];
     auto flag_of = [&](int m) {
@@ -179,6 +180,9 @@ __global__ void __launch_bounds__(256, 1)
                     // the tile's dispatch signal: its rows are in our heap
                     if (!wait_flag_geq(dflags + rt.tile_id, c.epoch, kWaitTimeoutNs))
                         atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                    if (c.trace && j.nb == 0)
+                        trace_seen(c, PERSEUS_EV_DISPATCH_SEEN, rt.src, rt.tile_id,
+                                   c.heap[c.rank] + (size_t(c.par) * c.R_max + rt.heap_row) * c.H, rt.rows);
                     fence_proxy_async();
                 }
                 for (int kb = 0; kb < g.num_kb; ++kb) {

@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
     if (lane == 0) {
         atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
         atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
+        if (c.trace) trace_ev(c, PERSEUS_EV_DISPATCH_PUT, st.dst, st.tile_id, st.group, uint32_t(st.rows) * c.H * 2, 0, fwd_now());
     }
     const Group g = c.groups[st.group];
     auto flag_of = [&](int m) {
@@ -382,9 +383,15 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
         const int e = c.ids[size_t(t) * k + v];
         if (e % c.P != c.rank) {
             const int32_t rel = c.pos[size_t(t) * k + v] - c.offsets[e];
-            const int tile = c.send[c.send_first[e] + rel / kTileRows].tile_id;
+            const int sp = c.send_first[e] + rel / kTileRows;
+            const int tile = c.send[sp].tile_id;
             if (!wait_flag_geq(c.cflag[c.rank] + size_t(c.par) * c.T_max + tile, c.epoch, kWaitTimeoutNs))
                 atomicAdd(&c.stats[kStatTimeouts], 1ull);
+            if (c.trace && atomicExch(c.trace_seen_ep + tile, c.epoch) != c.epoch) {
+                const SendTile st = c.send[sp];  // the tile's rows came back into our sorted slots
+                trace_seen(c, PERSEUS_EV_COMBINE_SEEN, st.dst, tile,
+                           c.ybuf[c.rank] + (size_t(c.par) * c.Y_rows + c.offsets[e] + st.row0) * c.H, st.rows);
+            }
         }
     }
     __syncthreads();

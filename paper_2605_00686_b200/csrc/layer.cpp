@@ -129,6 +129,9 @@ struct perseus_layer {
     uint32_t *send_done = nullptr, *g1_done = nullptr, *self_ready = nullptr, *sched = nullptr;
     unsigned long long* fwd_t = nullptr;
     unsigned long long* tl = nullptr;  // kernel timeline (perseus_layer_set_timeline)
+    TraceEv* trace = nullptr;          // device event log (perseus_layer_set_trace)
+    uint32_t *trace_n = nullptr, *trace_seen_ep = nullptr;
+    uint32_t trace_cap = 0;
     int32_t* send_first = nullptr;
     bool fused = true;  // forward() uses the fused persistent kernel
     bool stage_timing = false, timed_last = false;  // per-stage CUDA events (perseus_layer_set_stage_timing)
@@ -181,7 +184,8 @@ struct perseus_layer {
         c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
         c.max_send = max_send; c.max_recv = max_recv;
         c.sorder = sorder; c.rorder = rorder; c.send_done = send_done; c.g1_done = g1_done;
-        c.self_ready = self_ready; c.sched = sched; c.fwd_t = fwd_t; c.tl = tl; c.send_first = send_first; c.pairs = pairs;
+        c.self_ready = self_ready; c.sched = sched; c.fwd_t = fwd_t; c.tl = tl;
+        c.trace = trace; c.trace_n = trace_n; c.trace_cap = trace_cap; c.trace_seen_ep = trace_seen_ep; c.send_first = send_first; c.pairs = pairs;
         c.stats = stats;
         return c;
     }
@@ -227,7 +231,7 @@ void free_layer(perseus_layer* L) {
     void* ptrs[] = {L->x_stage, L->out_stage, L->wg, L->w1, L->w2, L->hbuf, L->logits, L->weights, L->ids,
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
-                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl, L->smaps,
+                    L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl, L->smaps, L->trace, L->trace_n, L->trace_seen_ep,
                     L->send_first, L->pairs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -290,6 +294,15 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     if (all) L->timed_last = tev;
     if (tev) ck(cudaEventRecord(L->ev[0], st), "event");
     if (all && L->tl) ck(cudaMemsetAsync(L->tl, 0, 2 * kTlCount * sizeof(unsigned long long), st), "memset");
+    if (L->trace && (all || phase == PERSEUS_PHASE_ROUTE)) {
+        // trace mode: empty event log, and this forward's receive buffers
+        // poisoned (bf16 0xFFFF) so a tile seen before its data shows up
+        ck(cudaMemsetAsync(L->trace_n, 0, sizeof(uint32_t), st), "memset");
+        ck(cudaMemsetAsync(L->sym + L->off_heap + size_t(c.par) * L->R_max * L->H * 2, 0xff,
+                           size_t(L->R_max) * L->H * 2, st), "poison heap");
+        ck(cudaMemsetAsync(L->sym + L->off_ybuf + size_t(c.par) * L->Y_rows * L->H * 2, 0xff,
+                           size_t(L->Y_rows) * L->H * 2, st), "poison ybuf");
+    }
     // Reference routing modes: the expert ids do not depend on the logits, so the
     // router GEMM runs on a side stream, overlapped with route/permute/plan, and
     // only the routing weights (written by the fused kernel) wait for it.
@@ -726,6 +739,44 @@ int perseus_layer_read_timeline(perseus_layer* L, uint64_t* start_end, int n) {
             start_end[2 * i] = h[2 * i] ? ~h[2 * i] : 0;
             start_end[2 * i + 1] = h[2 * i + 1];
         }
+    });
+}
+
+int perseus_layer_set_trace(perseus_layer* L, int on) {
+    return guarded([&] {
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        if (on && !L->trace) {
+            L->trace_cap = uint32_t(8 * (int64_t(L->max_send) + L->max_recv) + 1024);
+            ck(cudaMalloc(&L->trace, size_t(L->trace_cap) * sizeof(TraceEv)), "cudaMalloc trace");
+            ck(cudaMalloc(&L->trace_n, sizeof(uint32_t)), "cudaMalloc");
+            ck(cudaMemset(L->trace_n, 0, sizeof(uint32_t)), "memset");
+            ck(cudaMalloc(&L->trace_seen_ep, size_t(L->T_max) * sizeof(uint32_t)), "cudaMalloc");
+            ck(cudaMemset(L->trace_seen_ep, 0, size_t(L->T_max) * sizeof(uint32_t)), "memset");
+        } else if (!on && L->trace) {
+            cudaFree(L->trace);
+            cudaFree(L->trace_n);
+            cudaFree(L->trace_seen_ep);
+            L->trace = nullptr;
+            L->trace_n = L->trace_seen_ep = nullptr;
+            L->trace_cap = 0;
+        }
+    });
+}
+
+int perseus_layer_read_trace(perseus_layer* L, perseus_trace_event* events, size_t cap, size_t* n) {
+    static_assert(sizeof(perseus_trace_event) == sizeof(TraceEv), "trace event layout");
+    return guarded([&] {
+        if (!L->trace) throw sigsim::ConfigError("trace mode is off");
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");
+        uint32_t cnt = 0;
+        ck(cudaMemcpy(&cnt, L->trace_n, sizeof cnt, cudaMemcpyDeviceToHost), "memcpy");
+        if (cnt > L->trace_cap) throw sigsim::ModelError("device event log overflowed");
+        *n = cnt;
+        if (events && cap)
+            ck(cudaMemcpy(events, L->trace, std::min<size_t>(cap, cnt) * sizeof(TraceEv), cudaMemcpyDeviceToHost),
+               "memcpy trace");
     });
 }
 

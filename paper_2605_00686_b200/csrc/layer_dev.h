@@ -73,6 +73,10 @@ struct DevCtx {
 
     unsigned long long* stats;  // [kStatCount]
     unsigned long long* fwd_t;  // [kFwdSlots]: this forward's communication timestamps (P > 1)
+    TraceEv* trace;             // device event log (trace mode) or null
+    uint32_t* trace_n;          // events recorded this forward
+    uint32_t trace_cap;
+    uint32_t* trace_seen_ep;    // [T_max] combine tiles already observed this forward (epoch-valued)
     unsigned long long* tl;     // [2 * kTlCount] kernel timeline of the last forward (~start, end) or null
 };
 
@@ -112,6 +116,50 @@ __device__ __forceinline__ void tl_start(const DevCtx& c, int id) {
 }
 __device__ __forceinline__ void tl_end(const DevCtx& c, int id, bool me) {
     if (c.tl && me && blockIdx.x + 4 >= gridDim.x) atomicMax(c.tl + 2 * id + 1, fwd_now());
+}
+
+// Append one event to the device event log (trace mode only).
+__device__ __forceinline__ void trace_ev(const DevCtx& c, int kind, int peer, int tile, int group, uint32_t bytes,
+                                         uint32_t aux, uint64_t t) {
+    if (!c.trace) return;
+    const uint32_t i = atomicAdd(c.trace_n, 1u);
+    if (i >= c.trace_cap) return;
+    TraceEv e;
+    e.t = t;
+    e.kind = kind;
+    e.pe = c.rank;
+    e.peer = peer;
+    e.tile = tile;
+    e.group = group;
+    e.bytes = bytes;
+    e.aux = aux;
+    e.pad = 0;
+    c.trace[i] = e;
+}
+
+// Receiver side, trace mode: a remote tile's flag has just been seen; check
+// its rows (first and last 16 bytes of each) for the poison the receive
+// buffers were filled with before the forward.  Incomplete content = the
+// signal became visible before the data: wait for it, record both times.
+__device__ __forceinline__ void trace_seen(const DevCtx& c, int kind, int src, int tile, const bf16* rows0, int rows) {
+    const uint64_t t_seen = fwd_now();
+    auto complete = [&]() {
+        for (int r = 0; r < rows; ++r) {
+            const uint4* p = reinterpret_cast<const uint4*>(rows0 + size_t(r) * c.H);
+            const uint4 a = __ldcv(p), b = __ldcv(p + c.H / 8 - 1);
+            if ((a.x & a.y & a.z & a.w) == 0xffffffffu || (b.x & b.y & b.z & b.w) == 0xffffffffu) return false;
+        }
+        return true;
+    };
+    const bool ok = complete();
+    uint64_t t_land = t_seen;
+    if (!ok) {
+        while (!complete() && fwd_now() - t_seen < 1000000000ull) {
+        }
+        t_land = fwd_now();
+    }
+    trace_ev(c, kind, src, tile, -1, uint32_t(t_land - t_seen > 0xffffffffull ? 0xffffffffull : t_land - t_seen), ok ? 1u : 0u,
+             t_seen);
 }
 
 // Routing weights of token t: softmax over its k chosen experts' logits (the

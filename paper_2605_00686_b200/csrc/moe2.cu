@@ -132,6 +132,7 @@ __device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, i
     if (lane == 0) {
         atomicAdd(&c.stats[kStatCombinePuts], 1ull);
         atomicAdd(&c.stats[kStatCombineBytes], (unsigned long long)rt.rows * c.H * 2);
+        if (c.trace) trace_ev(c, PERSEUS_EV_COMBINE_PUT, rt.src, rt.tile_id, rt.cgroup, uint32_t(rt.rows) * c.H * 2, 0, fwd_now());
     }
     const Group grp = c.cgroups[rt.cgroup];
     auto flag_of = [&](int m) {
@@ -237,13 +238,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             struct Op {
                 const CUtensorMap* ta;
                 const CUtensorMap* tb;
-                int32_t a_row, b_row, nkb, kind, mine;
+                int32_t a_row, b_row, nkb, kind, mine, dup;
             };
             auto op_of = [&](int w) {
                 const Item it = item_of(w, T, f);
                 const int t0 = c.pairs[2 * it.t], t1 = c.pairs[2 * it.t + 1];
                 Op o;
                 o.mine = (crank == 0 || t1 < 0) ? t0 : t1;
+                o.dup = crank != 0 && t1 < 0;  // odd pair: the peer CTA recomputes t0's rows
                 const RecvTile rt = c.recv[o.mine];
                 o.kind = it.kind;
                 if (it.kind == 1) {
@@ -280,6 +282,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                     const uint64_t dw = globaltimer() - tw0;
                     wait_d += dw;
                     if (tile_id >= 0) wait_r += dw;
+                    if (c.trace && tile_id >= 0 && !cur.dup) {
+                        const RecvTile rt = c.recv[cur.mine];
+                        trace_seen(c, PERSEUS_EV_DISPATCH_SEEN, rt.src, tile_id,
+                                   c.heap[c.rank] + (size_t(c.par) * c.R_max + rt.heap_row) * c.H, rt.rows);
+                    }
                 } else {
                     if (!wait_flag_geq(c.g1_done + cur.mine, uint32_t(f.n1), kWaitTimeoutNs))
                         atomicAdd(&c.stats[kStatTimeouts], 1ull);
@@ -423,6 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (lane == 0) {
                 atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
                 atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
+                if (c.trace) trace_ev(c, PERSEUS_EV_DISPATCH_PUT, st.dst, st.tile_id, st.group, uint32_t(st.rows) * c.H * 2, 0, fwd_now());
             }
             const Group g = c.groups[st.group];
             auto flag_of = [&](int m) {

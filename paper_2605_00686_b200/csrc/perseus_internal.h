@@ -115,6 +115,21 @@ enum StatSlot : int {
     kStatCount
 };
 
+// Device event log (trace mode): what the kernels actually did, in the
+// reference's evidence vocabulary (trace.hpp:12-69); see perseus.h
+// perseus_trace_event for the host view and planner.cpp for the adapter.
+struct TraceEv {
+    uint64_t t;       // globaltimer ns of the recording PE
+    int32_t kind;     // PERSEUS_EV_*
+    int32_t pe;       // recording PE
+    int32_t peer;     // sender events: destination; receiver events: source
+    int32_t tile;     // reference tile id (flag id); -1 for fences
+    int32_t group;    // signal group of the sender (-1: none)
+    uint32_t bytes;   // puts: payload bytes; observes: ns from signal seen to content complete
+    uint32_t aux;     // signals: 1 = first flag after the group's fence; observes: 1 = content complete when seen
+    uint32_t pad;
+};
+
 // Per-forward communication timestamps (globaltimer ns), reset by the plan
 // kernel and folded into the stats by the combine kernel's last CTA.
 enum FwdSlot : int {

@@ -166,6 +166,23 @@ class MoELayer:
 
     TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2")
 
+    def set_trace(self, on: bool = True) -> None:
+        """Device event log of every following forward (puts, fences, flag writes,
+        receiver-side first observations with a content check; receive buffers
+        are poisoned per forward).  Diagnostics: costs time."""
+        check(lib.perseus_layer_set_trace(self._h, int(bool(on))))
+
+    def trace(self) -> np.ndarray:
+        """Events of the last forward as a structured array (perseus_trace_event)."""
+        n = C.c_size_t(0)
+        check(lib.perseus_layer_read_trace(self._h, None, 0, C.byref(n)))
+        buf = (_lib.TraceEvent * max(1, n.value))()
+        check(lib.perseus_layer_read_trace(self._h, buf, n.value, C.byref(n)))
+        dt = np.dtype([("t", np.uint64), ("kind", np.int32), ("pe", np.int32), ("peer", np.int32),
+                       ("tile", np.int32), ("group", np.int32), ("bytes", np.uint32), ("aux", np.uint32),
+                       ("pad", np.uint32)])
+        return np.frombuffer(bytes(buf), dtype=dt, count=n.value).copy()
+
     def set_timeline(self, on: bool = True) -> None:
         """Record a per-kernel device timeline of the following forwards (diagnostics)."""
         check(lib.perseus_layer_set_timeline(self._h, int(bool(on))))
@@ -196,3 +213,20 @@ class MoELayer:
             self.close()
         except Exception:
             pass
+
+
+def analyze_trace(events: np.ndarray, protocol: ProtocolConfig, transfers: np.ndarray) -> dict:
+    """One forward's device events (all PEs, concatenated) -> sigsim::RunTrace per
+    direction -> the reference's fence_accounting / verify_ordering /
+    conservation_check (perseus_trace_analyze).  `transfers`: the realised
+    dispatch transfers of all PEs (MoELayer.layout()[0] rows, concatenated)."""
+    ev = np.ascontiguousarray(events)
+    n = len(ev)
+    ebuf = (_lib.TraceEvent * max(1, n)).from_buffer_copy(ev.tobytes() or bytes(C.sizeof(_lib.TraceEvent)))
+    tr = np.asarray(transfers, dtype=np.int64).reshape(-1, 6)
+    tbuf = (_lib.Transfer * max(1, len(tr)))()
+    for i, row in enumerate(tr):
+        tbuf[i] = _lib.Transfer(int(row[0]), int(row[1]), int(row[2]), int(row[3]), int(row[4]), int(row[5]))
+    rep = _lib.TraceReport()
+    check(lib.perseus_trace_analyze(ebuf, n, int(protocol.ordering == "nic_fence"), tbuf, len(tr), C.byref(rep)))
+    return rep.as_dict()

@@ -10,7 +10,7 @@ def bf16_bits(t):
     return t.detach().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-def run_emulated(pb, model, S, P, routing="balanced", skew=0.0, seed=1, protocol=None, reps=1):
+def run_emulated(pb, model, S, P, routing="balanced", skew=0.0, seed=1, protocol=None, reps=1, before=None):
     """P EP ranks emulated on ONE device: phase p of every rank completes
     before phase p+1 of any rank (no cross-launch spin-waits on one GPU)."""
     import torch
@@ -18,6 +18,8 @@ def run_emulated(pb, model, S, P, routing="balanced", skew=0.0, seed=1, protocol
                           protocol=protocol) for r in range(P)]
     if P > 1:
         pb.MoELayer.connect_local(layers)
+    if before is not None:
+        before(layers)
     xs = [torch.empty(S, model.hidden_dim, dtype=torch.bfloat16, device="cuda") for _ in range(P)]
     outs = [torch.zeros_like(x) for x in xs]
     for r, l in enumerate(layers):

@@ -235,3 +235,42 @@ def test_forward_host_async_pipeline_matches_blocking(oracle):
     for i in range(4):
         assert np.array_equal(outs[i], want[i]), i
     l.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,proto", [(2, "vanilla"), (2, "combined"), (4, "decoupled"), (4, "combined")])
+def test_device_trace_to_reference_runtrace(oracle, P, proto):
+    """Device event log -> sigsim::RunTrace -> the reference's fence_accounting,
+    verify_ordering and conservation_check (metrics.cpp:10-59,118-190): fence
+    markers (ProxyFence) or flagged signals (NicFence) equal the reference's
+    per-PE fence accounting of the realised layout, no signal is seen before
+    its data, and every put tile is submitted, delivered and signalled once."""
+    from tests.gpu_util import run_emulated
+    pb = _pb()
+    E = 8 * P if P > 2 else 8
+    m = _model(pb, 256, 256, E, 2)
+    protocol = {"vanilla": pb.vanilla_protocol(), "combined": pb.combined_protocol(0),
+                "decoupled": pb.decoupled_protocol(0)}[proto]
+    layers, xs, outs = run_emulated(pb, m, 256, P, routing="zipf", skew=1.0, seed=7, protocol=protocol,
+                                    before=lambda ls: [l.set_trace(True) for l in ls])
+    events = np.concatenate([l.trace() for l in layers])
+    transfers = np.concatenate([l.layout()[0] for l in layers])
+    rep = pb.analyze_trace(events, protocol, transfers)
+    counters = [l.counters() for l in layers]
+    nic = protocol.ordering == "nic_fence"
+    for d, key in ((0, "dispatch"), (1, "combine")):
+        dev_fences = sum(c[f"{key}_fences"] for c in counters)
+        r = rep[key]
+        assert (r["flagged_signal_count"] if nic else r["fence_count"]) == dev_fences, (key, r, dev_fences)
+        assert (r["fence_count"] if nic else r["flagged_signal_count"]) == 0, (key, r)
+        assert r["ordering_violations"] == 0 and r["late_tiles"] == 0, (key, r)
+        assert r["conservation_ok"], rep["conservation_error"]
+        assert r["put_bytes"] == int(transfers[:, 3].sum())
+    # dispatch fences vs the reference's accounting of the same layout
+    tr = transfers[np.lexsort((transfers[:, 4], transfers[:, 2], transfers[:, 1], transfers[:, 0]))]
+    mode = 0 if protocol.signaling == "coupled" else 1
+    want = sum(oracle.fences_for_src(tr[tr[:, 0] == s], s, mode, 0) for s in range(P))
+    got = rep["dispatch"]["flagged_signal_count" if nic else "fence_count"]
+    assert got == want, (got, want)
+    for l in layers:
+        l.close()
