@@ -238,7 +238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             struct Op {
                 const CUtensorMap* ta;
                 const CUtensorMap* tb;
-                int32_t a_row, b_row, nkb, kind, mine, dup;
+                int32_t a_row, b_row, nkb, kind, mine, dup, nb;
             };
             auto op_of = [&](int w) {
                 const Item it = item_of(w, T, f);
@@ -246,6 +246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 Op o;
                 o.mine = (crank == 0 || t1 < 0) ? t0 : t1;
                 o.dup = crank != 0 && t1 < 0;  // odd pair: the peer CTA recomputes t0's rows
+                o.nb = it.nb;
                 const RecvTile rt = c.recv[o.mine];
                 o.kind = it.kind;
                 if (it.kind == 1) {
@@ -282,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                     const uint64_t dw = globaltimer() - tw0;
                     wait_d += dw;
                     if (tile_id >= 0) wait_r += dw;
-                    if (c.trace && tile_id >= 0 && !cur.dup) {
+                    if (c.trace && tile_id >= 0 && !cur.dup && cur.nb == 0) {  // first n-block's observation
                         const RecvTile rt = c.recv[cur.mine];
                         trace_seen(c, PERSEUS_EV_DISPATCH_SEEN, rt.src, tile_id,
                                    c.heap[c.rank] + (size_t(c.par) * c.R_max + rt.heap_row) * c.H, rt.rows);

@@ -81,9 +81,52 @@ def main():
         results.append(all_r)
         layer.close()
         dist.barrier()
+    # ---- device event log of real concurrent forwards -> the reference's RunTrace checks ----
+    # Safe protocols must show no signal seen before its data; the fault-injection
+    # variant (flags without the fence, transport.cpp:104-106) is reported.
+    traces = []
+    H, I, E, k, S = 2048, 768, 16 * world, 8, 2048
+    for proto in (pb.combined_protocol(0), pb.vanilla_protocol(),
+                  pb.ProtocolConfig(signaling="decoupled", ordering="nic_fence", suppress_fences=True),
+                  pb.ProtocolConfig(signaling="coupled", suppress_fences=True)):
+        m = pb.ModelConfig("m", H, I, E, k)
+        layer = pb.MoELayer(m, S, rank=rank, world=world, device=local, routing="balanced", seed=3, protocol=proto)
+        layer.connect_dist()
+        x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
+        out = torch.empty_like(x)
+        layer.fill_synthetic_x(x, 3)
+        layer.forward(x, out)
+        layer.set_trace(True)
+        reps = []
+        for _ in range(5):
+            torch.cuda.synchronize()
+            dist.barrier()
+            layer.forward(x, out)
+            torch.cuda.synchronize()
+            ev = [None] * world
+            tr = [None] * world
+            dist.all_gather_object(ev, layer.trace())
+            dist.all_gather_object(tr, layer.layout()[0])
+            if rank == 0:
+                reps.append(pb.analyze_trace(np.concatenate(ev), proto, np.concatenate(tr)))
+        layer.set_trace(False)
+        layer.close()
+        dist.barrier()
+        if rank == 0:
+            safe = not proto.suppress_fences
+            viol = [r["dispatch"]["ordering_violations"] + r["combine"]["ordering_violations"] for r in reps]
+            cons = all(r["dispatch"]["conservation_ok"] and r["combine"]["conservation_ok"] for r in reps)
+            entry = {"protocol": proto.mode_name() + ("+no_fence" if proto.suppress_fences else ""),
+                     "forwards": len(reps), "violations": viol, "conservation": cons,
+                     "dispatch": reps[-1]["dispatch"], "combine": reps[-1]["combine"]}
+            if safe and (any(viol) or not cons):
+                ok = False
+                entry["ok"] = False
+            traces.append(entry)
     if rank == 0:
-        verdict = all(rr["ok"] for res in results for rr in res)
-        print(json.dumps({"mgpu_check": "pass" if verdict else "FAIL", "world": world, "results": results}))
+        verdict = ok and all(rr["ok"] for res in results for rr in res)
+        print(json.dumps({"mgpu_check": "pass" if verdict else "FAIL", "world": world, "results": results,
+                          "device_trace": traces}))
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 
