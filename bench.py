@@ -413,11 +413,17 @@ def main():
                  "tensor": {"achieved_tflops": ach_tf, "frac": ach_tf / tflops_peak},
                  "hbm": {"achieved_gbs": ach_gb, "frac": ach_gb / hbm_peak},
                  "timing": "CUDA events on the layer stream around the kernel, mean of 10 synchronised steps"})
-    # layer roofline: slowest of tensor-at-peak, HBM bytes and bytes-over-NVLink (770 GB/s/direction measured)
+    # layer roofline: slowest of tensor-at-peak, HBM bytes and bytes-over-NVLink (measured peer-store ceiling)
     flops_layer = 6.0 * H * I * S * k + 2.0 * S * H * E
     nvl_bytes = 2.0 * S * k * (world - 1) / world * H * 2
     hbm_layer = (E // world) * 3.0 * H * I * 2 + 2.0 * rows * H * 2 + 2.0 * rows * I * 2 + 2.0 * rows * H * 2
-    t_roof = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / 770e9, hbm_layer / (hbm_peak * 1e9))
+    nvl_bw, nvl_src = 720e9, "assumed"
+    pp = os.path.join(ROOT, "profiles", "r01_nvlink_p2p_bw.json")
+    if os.path.exists(pp):
+        with open(pp) as fh:
+            nvl_bw = max(r["GBps"] for r in json.load(fh)["results"] if r["mode"] == "sm_st16") * 1e9
+        nvl_src = "profiles/r01_nvlink_p2p_bw.json (measured SM peer stores)"
+    t_roof = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / nvl_bw, hbm_layer / (hbm_peak * 1e9))
     layer_frac = t_roof / (ms_step / 1e3)
 
     cpu = None
@@ -487,7 +493,8 @@ def main():
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes, "hbm_bytes": hbm_layer,
                                "t_tensor_us": flops_layer / (tflops_peak * 1e12) * 1e6,
-                               "t_nvlink_us": nvl_bytes / 770e9 * 1e6,
+                               "t_nvlink_us": nvl_bytes / nvl_bw * 1e6, "nvlink_gbs": nvl_bw / 1e9,
+                               "nvlink_source": nvl_src,
                                "t_hbm_us": hbm_layer / (hbm_peak * 1e9) * 1e6},
             "roofline": roof,
             "comm": comm,
