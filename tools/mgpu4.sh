@@ -13,3 +13,4 @@ print("comm", json.dumps(d["comm"]))
 print("variant", json.dumps(d["per_tile_fence_variant"]))
 print("timeline", json.dumps(d["timeline_us"]))
 PY
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29513 tools/nccl_baseline.py 2>&1 | grep '^{' | tee gpurun_out/nccl_n$N.json
