@@ -239,6 +239,11 @@ int perseus_layer_read_count_table(perseus_layer* layer, int32_t* table);
 int perseus_layer_set_timeline(perseus_layer* layer, int on);
 int perseus_layer_read_timeline(perseus_layer* layer, uint64_t* start_end, int n_kernels);
 
+/* replaces sigsim::fit_alpha_beta (metrics.hpp, metrics.cpp:69-95): least-squares
+ * t = alpha + beta * bytes over n >= 2 points (ConfigError if degenerate). */
+int perseus_fit_alpha_beta(const double* bytes, const double* ns, size_t n, double* alpha_ns,
+                           double* beta_ns_per_byte, double* r_squared);
+
 /* ---- device event log (trace mode) -> the reference's RunTrace ----------
  * With tracing on, every forward records what the kernels actually did:
  * sender-side puts, fences and flag writes, and receiver-side observations of

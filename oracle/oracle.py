@@ -351,6 +351,8 @@ class RefLib:
         L = C.CDLL(REF_SO)
         self.L = L
         L.ref_last_error.restype = C.c_char_p
+        L.ref_fit_alpha_beta.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t,
+                                         C.POINTER(C.c_double)]
         L.ref_remote_transfer_count.argtypes = [C.c_int64] * 3 + [C.POINTER(C.c_int64)]
         L.ref_message_size.restype = C.c_uint64
         L.ref_message_size.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64]
@@ -369,6 +371,14 @@ class RefLib:
         L.ref_fnv1a64.restype = C.c_uint64
         L.ref_fnv1a64.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64]
 
+
+    def fit_alpha_beta(self, points):
+        xs = (C.c_double * len(points))(*[p[0] for p in points])
+        ys = (C.c_double * len(points))(*[p[1] for p in points])
+        out = (C.c_double * 3)()
+        if self.L.ref_fit_alpha_beta(xs, ys, len(points), out) != 0:
+            raise ValueError(self.L.ref_last_error().decode())
+        return tuple(out)
     def _chk(self, rc):
         if rc == 1:
             raise ValueError("ConfigError: " + self.L.ref_last_error().decode())

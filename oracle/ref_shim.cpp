@@ -185,6 +185,19 @@ int ref_run_dispatch(int mode, int64_t group_size, int64_t H, int64_t I, int64_t
     });
 }
 
+#define COMMA ,
+// sigsim::fit_alpha_beta (metrics.cpp:69-95); out = {alpha_ns, beta_ns_per_byte, r_squared}
+int ref_fit_alpha_beta(const double* x, const double* y, size_t n, double* out) {
+    REF_TRY({
+        std::vector<std::pair<double COMMA double>> pts(n);
+        for (size_t i = 0; i < n; ++i) pts[i] = std::make_pair(x[i] COMMA y[i]);
+        auto f = sigsim::fit_alpha_beta(pts);
+        out[0] = f.alpha_ns;
+        out[1] = f.beta_ns_per_byte;
+        out[2] = f.r_squared;
+    });
+}
+
 // fnv1a64 (trace.cpp:53-62)
 uint64_t ref_fnv1a64(const void* data, size_t len, uint64_t h) {
     return sigsim::fnv1a64(data, len, h);

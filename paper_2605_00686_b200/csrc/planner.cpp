@@ -595,6 +595,18 @@ int perseus_trace_analyze(const perseus_trace_event* ev, size_t n, int nic_order
     });
 }
 
+int perseus_fit_alpha_beta(const double* bytes, const double* ns, size_t n, double* alpha_ns,
+                           double* beta_ns_per_byte, double* r_squared) {
+    return guarded([&] {
+        std::vector<std::pair<double, double>> pts(n);
+        for (size_t i = 0; i < n; ++i) pts[i] = {bytes[i], ns[i]};
+        const auto f = sigsim::fit_alpha_beta(pts);
+        *alpha_ns = f.alpha_ns;
+        *beta_ns_per_byte = f.beta_ns_per_byte;
+        *r_squared = f.r_squared;
+    });
+}
+
 uint64_t perseus_fnv1a64(const void* data, size_t len, uint64_t h) {
     return sigsim::fnv1a64(data, len, h);
 }

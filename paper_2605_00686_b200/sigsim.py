@@ -19,7 +19,7 @@ __all__ = ["ModelConfig", "ClusterConfig", "TransferSpec", "DispatchWorkload", "
            "ProtocolConfig", "model_preset", "model_preset_names", "remote_transfer_count",
            "message_size", "zipf_route", "build_dispatch", "assign_groups", "heap_digest",
            "fnv1a64", "vanilla_protocol", "decoupled_protocol", "nic_ordering_protocol",
-           "combined_protocol", "gpu_direct_protocol", "expected_fences"]
+           "combined_protocol", "gpu_direct_protocol", "expected_fences", "fit_alpha_beta"]
 
 
 @dataclass
@@ -233,3 +233,13 @@ def expected_fences(protocol: ProtocolConfig, wl: DispatchWorkload, src_pe: int)
     if protocol.signaling == "coupled":
         return len(own)
     return len(assign_groups(own, protocol.group_size)) if own else 0
+
+
+def fit_alpha_beta(points):
+    """sigsim::fit_alpha_beta (metrics.cpp:69-95): least-squares t = alpha + beta*bytes
+    over [(bytes, ns), ...]; returns (alpha_ns, beta_ns_per_byte, r_squared)."""
+    xs = (C.c_double * len(points))(*[float(p[0]) for p in points])
+    ys = (C.c_double * len(points))(*[float(p[1]) for p in points])
+    a, b, r2 = C.c_double(), C.c_double(), C.c_double()
+    check(lib.perseus_fit_alpha_beta(xs, ys, len(points), C.byref(a), C.byref(b), C.byref(r2)))
+    return a.value, b.value, r2.value

@@ -120,3 +120,24 @@ def test_planner_agrees_with_oracle_on_random_layouts(oracle):
         rem, loc, dig = oracle.build_dispatch(H, E, k, P, 1, S, skew, tb, 17)
         assert wl.digest() == dig
         assert np.array_equal(wl.remote_array(), rem)
+
+
+def test_fit_alpha_beta_matches_reference():
+    """perseus_fit_alpha_beta == sigsim::fit_alpha_beta of the reference library
+    (metrics.cpp:69-95) on random message-size / time points, incl. the error case."""
+    import pytest as _pt
+    from oracle.oracle import RefLib
+    if not RefLib.available():
+        _pt.skip("reference library not built")
+    ref = RefLib()
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        n = int(rng.integers(2, 12))
+        pts = [(float(rng.integers(1, 1 << 24)), float(rng.random() * 1e6)) for _ in range(n)]
+        if len({p[0] for p in pts}) == 1:
+            continue
+        got = pb.fit_alpha_beta(pts)
+        want = ref.fit_alpha_beta(pts)
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-9), (got, want)
+    with _pt.raises(pb.ConfigError):
+        pb.fit_alpha_beta([(5.0, 1.0), (5.0, 2.0)])

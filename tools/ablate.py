@@ -12,6 +12,7 @@ against the reference's fence accounting of the same layout (ClusterConfig
 (max over ranks).  Rank 0 writes a versioned CSV (runner.cpp:29-58 style).
 """
 import argparse
+import json
 import os
 import sys
 import time
@@ -28,9 +29,10 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", default="256,1024,4096,16384")
-    ap.add_argument("--modes", default="vanilla,perseus,gs8")
+    ap.add_argument("--modes", default="vanilla,perseus,gsdiv",
+                    help="vanilla | perseus (per destination) | gsN | gsdiv (every power-of-two divisor)")
     ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ablation.csv"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "ablation.csv"))
     args = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -44,7 +46,18 @@ def main():
     for S in [int(s) for s in args.tokens.split(",")]:
         # the reference's layout and fence accounting for this point
         wl = pb.build_dispatch(model, pb.ClusterConfig(world, 1, 1), S, 0.0, 128 * H * 2, 1)
+        n_own0 = sum(1 for t in wl.remote_transfers if t.src_pe == rank)
+        modes = []
         for mode in args.modes.split(","):
+            if mode == "gsdiv":  # group-size sweep over the divisors (assign_groups gs > 0)
+                g = 2
+                while g < n_own0:
+                    if n_own0 % g == 0:
+                        modes.append(f"gs{g}")
+                    g *= 2
+            else:
+                modes.append(mode)
+        for mode in modes:
             if mode == "vanilla":
                 proto = pb.vanilla_protocol()
             elif mode == "perseus":
@@ -76,7 +89,9 @@ def main():
             c1 = layer.counters()
             d = {k: (c1[k] - c0[k]) / args.steps for k in c1}
             assert d["wait_timeouts"] == 0 and d["errors"] == 0, d
+            own_bytes = sum(t.bytes for t in wl.remote_transfers if t.src_pe == rank)
             row = dict(P=world, S=S, mode=proto.mode_name() + (f"_gs{proto.group_size}" if proto.group_size else ""),
+                       bytes=own_bytes,
                        dispatch_fences=d["dispatch_fences"], combine_fences=d["combine_fences"],
                        ref_fences=ref_f, signals=d["dispatch_signals"], us=float(ms.item()) * 1e3,
                        tokens_per_s=world * S / (float(ms.item()) / 1e3),
@@ -93,15 +108,32 @@ def main():
             layer.close()
             dist.barrier()
     if rank == 0:
+        # alpha-beta fit per mode: forward time vs this PE's dispatch bytes over S
+        # (fit_alpha_beta, metrics.cpp:69-95)
+        fits = {}
+        by_mode = {}
+        for allrows in rows:
+            r0 = allrows[0]
+            by_mode.setdefault(r0["mode"], []).append((float(r0["bytes"]), r0["us"] * 1e3))
+        for mode, pts in by_mode.items():
+            if len({p[0] for p in pts}) >= 2:
+                a, b, r2 = pb.fit_alpha_beta(pts)
+                fits[mode] = {"alpha_us": a / 1e3, "beta_ns_per_byte": b, "GBps_equiv": (1.0 / b) if b > 0 else None,
+                              "r_squared": r2, "points": len(pts)}
+        fit_path = os.path.splitext(args.out)[0] + f"_fits_p{world}.json"
+        with open(fit_path, "w") as fh:
+            json.dump({"P": world, "fits": fits}, fh, indent=1)
+        print("alpha-beta fits:", json.dumps(fits), flush=True)
         new = not os.path.exists(args.out)
         with open(args.out, "a") as f:
             if new:
-                f.write("# schema=1 perseus-b200 signalling ablation (BASELINE configs[4]); per-PE fences per forward;"
-                        " time = max over ranks, CUDA events\n")
-                f.write("P,S,mode,rank,dispatch_fences,combine_fences,reference_fences,match,us_per_forward,tokens_per_s\n")
+                f.write("# schema=2 perseus-b200 signalling ablation (BASELINE configs[4]); per-PE fences per forward;"
+                        " time = max over ranks, CUDA events; bytes = this PE's dispatch payload\n")
+                f.write("P,S,mode,rank,bytes,dispatch_fences,combine_fences,reference_fences,match,us_per_forward,"
+                        "tokens_per_s\n")
             for allrows in rows:
                 for rk, a in enumerate(allrows):
-                    f.write(f"{a['P']},{a['S']},{a['mode']},{rk},{a['dispatch_fences']:.0f},{a['combine_fences']:.0f},"
+                    f.write(f"{a['P']},{a['S']},{a['mode']},{rk},{a['bytes']},{a['dispatch_fences']:.0f},{a['combine_fences']:.0f},"
                             f"{a['ref_fences']},{a['match']},{a['us']:.1f},{a['tokens_per_s']:.0f}\n")
         print("wrote", args.out)
     dist.destroy_process_group()
