@@ -465,9 +465,9 @@ def main():
             "dispatch": variant["fences_per_forward"]["dispatch_fences"] / dc["dispatch_fences"],
             "combine": variant["fences_per_forward"]["combine_fences"] / max(dc["combine_fences"], 1e-9)}
         variant["slowdown_vs_this_run"] = variant["ms_per_step"] / ms_step
-    # our kernels per forward: router GEMM, k_route, k_perm, k_plan4, then k_moe2 (fused)
-    # or k_dispatch + k_gemm<1> + k_gemm<2> (unfused), then k_combine
-    launches_per_step = 6 if not args.unfused else 8
+    # our kernels per forward: router GEMM, k_route, k_perm (+ the plan CTA), then
+    # k_moe2 (fused) or k_dispatch + k_gemm<1> + k_gemm<2> (unfused), then k_combine
+    launches_per_step = 5 if not args.unfused else 7
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,

@@ -197,9 +197,19 @@ __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33
 __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     pdl_wait();
     pdl_launch_dependents();
-    tl_start(c, kTlPerm);
     extern __shared__ int32_t sm[];
-    const int E = c.E, b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
+    const int E = c.E, b = blockIdx.x, nb = int(gridDim.x) - c.with_plan, tid = threadIdx.x;
+    if (b == nb) {
+        // the plan CTA: waits for every PE's counts (this rank's from CTA 0 below)
+        // and builds the plan while the other CTAs rank their tokens
+        if (tid < 128) {
+            if (tid == 0 && c.tl) atomicMax(c.tl + 2 * kTlPlan, ~fwd_now());
+            plan_body(c, sm);
+            if (tid == 0 && c.tl) atomicMax(c.tl + 2 * kTlPlan + 1, fwd_now());
+        }
+        return;
+    }
+    tl_start(c, kTlPerm);
     uint32_t* bits = reinterpret_cast<uint32_t*>(sm);  // [E][kPermT / 32]
     int32_t* base = sm + E * (kPermT / 32);             // [E]
     int32_t* tot = base + E;                            // [E]
@@ -457,10 +467,14 @@ __global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
 }
 
 // route + permutation + count publish (after the gate logits exist)
-void launch_route(const DevCtx& c, cudaStream_t st) {
+// route + permutation + count publish (+ the plan, by one extra CTA of k_perm)
+void launch_route(const DevCtx& c, bool with_plan, cudaStream_t st) {
     launch_pdl(k_route, dim3((c.S + 7) / 8), dim3(256), 0, st, c);  // + block histograms
     const int nb = (c.S + kPermT - 1) / kPermT;
-    launch_pdl(k_perm, dim3(nb), dim3(kPermT), perm_smem_bytes(c), st, c);  // + count publish
+    DevCtx cc = c;
+    cc.with_plan = with_plan ? 1 : 0;
+    launch_pdl(k_perm, dim3(nb + cc.with_plan), dim3(kPermT), std::max(perm_smem_bytes(c), plan_smem_bytes(c)), st,
+               cc);  // + count publish
 }
 
 size_t perm_smem_bytes(const DevCtx& c) {
@@ -471,10 +485,7 @@ void launch_plan(const DevCtx& c, cudaStream_t st) {
     launch_pdl(k_plan4, dim3(1), dim3(128), plan_smem_bytes(c), st, c);
 }
 
-void launch_dispatch(const DevCtx& c, cudaStream_t st) {
-    launch_plan(c, st);
-    k_dispatch<<<c.max_send, 256, 0, st>>>(c);
-}
+void launch_dispatch(const DevCtx& c, cudaStream_t st) { k_dispatch<<<c.max_send, 256, 0, st>>>(c); }
 
 void launch_combine(const DevCtx& c, cudaStream_t st) {
     const int threads = c.H / 8;  // H <= 8192
@@ -499,7 +510,8 @@ static cudaError_t max_carveout(K* kernel) {
 cudaError_t configure_kernels(const DevCtx& c) {
     cudaError_t e = cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan_smem_bytes(c)));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(perm_smem_bytes(c)));
+    e = cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(std::max(perm_smem_bytes(c), plan_smem_bytes(c))));
     if (e != cudaSuccess) return e;
     const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_perm), max_carveout(k_plan4), max_carveout(k_dispatch),
                               max_carveout(k_gate), max_carveout(k_synth_fill), max_carveout(k_combine<0>),

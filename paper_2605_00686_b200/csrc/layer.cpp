@@ -24,7 +24,7 @@ namespace perseus {
 void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, float scale, cudaStream_t st);
 void launch_gate_exact(const DevCtx& c, cudaStream_t st);
 void launch_gate_tc(const CUtensorMap& tx, const CUtensorMap& twg, const DevCtx& c, int grid, cudaStream_t st);
-void launch_route(const DevCtx& c, cudaStream_t st);
+void launch_route(const DevCtx& c, bool with_plan, cudaStream_t st);
 void launch_plan(const DevCtx& c, cudaStream_t st);
 void launch_dispatch(const DevCtx& c, cudaStream_t st);
 cudaError_t configure_moe();
@@ -328,11 +328,10 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         } else {
             launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, st);
         }
-        launch_route(c, st);
+        launch_route(c, /*with_plan=*/all, st);
     }
     if (tev) ck(cudaEventRecord(L->ev[1], st), "event");
     if (all && L->fused) {
-        launch_plan(c, st);
         // one persistent kernel: dispatch puts + GEMM1 + GEMM2/combine puts,
         // overlapped tile by tile (gemm.cu:k_moe)
         if (side_gate) ck(cudaStreamWaitEvent(st, L->ev_gate, 0), "wait");  // router done before the persistent kernel
@@ -351,6 +350,7 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         ck(cudaGetLastError(), "kernel launch");
         return;
     }
+    if (phase == PERSEUS_PHASE_DISPATCH) launch_plan(c, st);  // all: built by k_perm's plan CTA
     if (all || phase == PERSEUS_PHASE_DISPATCH) launch_dispatch(c, st);
     if (tev) ck(cudaEventRecord(L->ev[2], st), "event");
     if (all || phase == PERSEUS_PHASE_EXPERT) {

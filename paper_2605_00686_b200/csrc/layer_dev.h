@@ -68,6 +68,7 @@ struct DevCtx {
     uint32_t* sched;      // [4]: work-item / copy-unit counters
     int32_t* send_first;  // [E]: first send position of each expert's tiles
     int32_t* pairs;       // [max_recv][2]: M-tile pairs (recv positions, -1 = none) in processing order
+    int32_t with_plan;    // k_perm: one extra CTA builds the plan
     int32_t self_head;    // minimum self pairs processed before the remote ones
     float head_ratio;     // est. link time of one tile / compute time of one M-tile pair
 
