@@ -397,6 +397,9 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->max_recv = int(int64_t(world) * (int64_t(L->S) * std::min(L->k, L->El) / kTileRows + L->El + 1));
             ck(cudaSetDevice(device), "cudaSetDevice");
             ck(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+            // PERSEUS_NUM_SMS: cap the persistent grids (several ranks sharing one GPU in
+            // oversubscribed multi-rank tests; each rank's fused kernel then fits beside the others)
+            if (const char* e = getenv("PERSEUS_NUM_SMS")) L->num_sms = std::max(2, std::min(L->num_sms, atoi(e)) & ~1);
             ck(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&L->stream2, cudaStreamNonBlocking), "stream2");
             ck(cudaEventCreateWithFlags(&L->ev_x, cudaEventDisableTiming), "event");

@@ -23,7 +23,8 @@ def main():
     import torch.distributed as dist
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # more ranks than GPUs (oversubscribed run with PERSEUS_NUM_SMS capping each rank's grids)
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     import paper_2605_00686_b200 as pb
