@@ -226,11 +226,25 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = max(1, torch.cuda.device_count())
+    oversub = world > ngpu  # more ranks than GPUs (tests only; PERSEUS_NUM_SMS caps each rank's grids)
+    local %= ngpu
     if world != args.gpus:
         args.gpus = world
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def allmax(v):
+        """max over ranks of a host float (NCCL on a device tensor; gloo on CPU when oversubscribed)"""
+        if world == 1:
+            return float(v)
+        t = torch.tensor([float(v)], device="cpu" if oversub else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     import paper_2605_00686_b200 as pb
 
@@ -276,10 +290,7 @@ def main():
     n_clk1 = len(clk.lines)
     ms = start.elapsed_time(end)
     c1 = layer.counters()
-    t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = allmax(ms)
     ms_step = ms_max / args.steps
     value = world * S * args.steps / (ms_max / 1e3)
 
@@ -320,10 +331,7 @@ def main():
         t0 = time.perf_counter()
         fn(steps)
         barrier()
-        dt = torch.tensor([time.perf_counter() - t0], device="cuda")
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        return float(dt.item())
+        return allmax(time.perf_counter() - t0)
 
     def run_async(n):
         for _ in range(n):
@@ -361,9 +369,7 @@ def main():
         ve.record(stream)
         barrier()
         v1 = vl.counters()
-        vt = torch.tensor([vs.elapsed_time(ve)], device="cuda")
-        dist.all_reduce(vt, op=dist.ReduceOp.MAX)
-        v_ms = float(vt.item()) / args.variant_steps
+        v_ms = allmax(vs.elapsed_time(ve)) / args.variant_steps
         vd = {key: (v1[key] - v0[key]) / args.variant_steps for key in ("dispatch_fences", "combine_fences")}
         variant = {"signaling": "coupled (per-tile fence), same fused kernel", "steps": args.variant_steps,
                    "ms_per_step": v_ms, "value": world * S / (v_ms / 1e3), "unit": "tokens/s",
