@@ -105,6 +105,9 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU arms ----
+_CPU_CACHE = {}
+
+
 def cpu_layer_sample(cfg, tokens, seed=1, P=1, threads=None):
     """One bounded step of the reference CPU path on the host cores: the
     reference's own dispatch/signalling path (oracle/_ref: build_dispatch +
@@ -117,11 +120,18 @@ def cpu_layer_sample(cfg, tokens, seed=1, P=1, threads=None):
     H, I, E, k = cfg["H"], cfg["I"], cfg["E"], cfg["k"]
     shape = LayerShape(H, I, E, k, tokens, P)
     ref = RefLib() if RefLib.available() else None
-    # resident inputs (not timed): tokens and this PE's bf16 weights
-    x = orc.gen_x(shape, seed, 0)
-    wg = orc.gen_wg(shape, seed)
-    w1 = [orc.gen_w1(shape, seed, e) for e in range(E)]
-    w2 = [orc.gen_w2(shape, seed, e) for e in range(E)]
+    # resident inputs (not timed, generated once): tokens and this PE's bf16 weights
+    wkey = (H, I, E, k, seed)
+    if _CPU_CACHE.get("wkey") != wkey:
+        _CPU_CACHE.clear()
+        _CPU_CACHE["wkey"] = wkey
+        # expert weights resident in fp32 (a CPU implementation keeps them so)
+        _CPU_CACHE["w"] = (orc.gen_wg(shape, seed), [orc.bf16_to_f32(orc.gen_w1(shape, seed, e)) for e in range(E)],
+                           [orc.bf16_to_f32(orc.gen_w2(shape, seed, e)) for e in range(E)])
+    if ("x", tokens) not in _CPU_CACHE:
+        _CPU_CACHE[("x", tokens)] = orc.gen_x(shape, seed, 0)
+    x = _CPU_CACHE[("x", tokens)]
+    wg, w1, w2 = _CPU_CACHE["w"]
     t0 = time.perf_counter()
     if ref is not None:
         r = ref.run_dispatch("combined", 0, H, I, E, k, max(P, 2), 1, 1, tokens, 0.0, 128 * H * 2, seed)
@@ -138,8 +148,7 @@ def cpu_layer_sample(cfg, tokens, seed=1, P=1, threads=None):
         a, b = int(off[e]), int(off[e + 1])
         if a == b:
             continue
-        w1f = orc.bf16_to_f32(w1[e])
-        w2f = orc.bf16_to_f32(w2[e])
+        w1f, w2f = w1[e], w2[e]
         xe = xf[rows[a:b]]
         g = xe @ w1f[:I].T
         u = xe @ w1f[I:].T
@@ -166,9 +175,19 @@ def run_reference_arm(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    tokens = args.ref_tokens
+    # bounded sample per step: calibrate the CPU path's per-token cost, then size
+    # each step so the whole --steps K run takes about --ref-budget-s seconds
+    cpu_layer_sample(cfg, 16)
+    _, t16, _, _ = cpu_layer_sample(cfg, 16)
+    _, t128, _, _ = cpu_layer_sample(cfg, 128)
+    per_token = max(1e-6, (t128 - t16) / 112)
+    fixed = max(0.0, t16 - 16 * per_token)
+    import math
+    q = cfg["E"] // math.gcd(cfg["E"], cfg["k"])  # balanced routing needs E | S*k (workload.cpp:165-168)
+    tokens = int((args.ref_budget_s / max(1, args.steps) - fixed) / per_token) // q * q
+    tokens = max(q, min(args.ref_tokens // q * q, tokens))
     for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_layer_sample(cfg, min(tokens, 128))
+        cpu_layer_sample(cfg, tokens)
     vals = []
     kind = desc = None
     t_all = time.perf_counter()
@@ -205,7 +224,8 @@ def main():
     ap.add_argument("--group-size", type=int, default=0, help="decoupled signal group size (0 = per destination PE)")
     ap.add_argument("--routing", default="balanced", choices=["balanced", "zipf", "gate"])
     ap.add_argument("--skew", type=float, default=0.0)
-    ap.add_argument("--ref-tokens", type=int, default=1024)
+    ap.add_argument("--ref-tokens", type=int, default=1024, help="max tokens per reference-arm step")
+    ap.add_argument("--ref-budget-s", type=float, default=90.0, help="reference arm: target seconds for all steps")
     ap.add_argument("--cpu-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="stage kernels instead of the fused persistent kernel")
