@@ -309,9 +309,9 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     static const bool side_ok = [] { const char* e = getenv("PERSEUS_SIDE_GATE"); return !e || atoi(e) != 0; }();
     const bool side_gate = side_ok && all && L->fused && L->cfg.routing != PERSEUS_ROUTE_GATE;
     c.weights_late = side_gate;
-    // pair order: the first ~two waves of GEMM1 items on self pairs, then the
-    // remote pairs (same lag as launch_moe2's item interleave)
-    c.self_head = std::max(1, (L->num_sms + L->I / 128 - 1) / (L->I / 128));
+    // pair order: at least one wave of GEMM1 items on self pairs before the
+    // remote pairs (the lag of launch_moe2's item interleave)
+    c.self_head = std::max(1, (L->num_sms / 2 + L->I / 128 - 1) / (L->I / 128));
     {
         const double t_tile = 128.0 * L->H * 2 / 600e9;                   // NVLink store rate per sender
         const double t_pair = 2.0 * 128 * 6.0 * L->H * L->I / 1.0e15;      // GPU-wide: pairs complete at ~1 PFLOP/s

@@ -283,6 +283,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                     const uint64_t dw = globaltimer() - tw0;
                     wait_d += dw;
                     if (tile_id >= 0) wait_r += dw;
+                    if (c.trace) trace_ev(c, kEvDiagItemWait, tile_id >= 0 ? c.recv[cur.mine].src : c.rank, cur.mine,
+                                          cur.nb, uint32_t(dw), uint32_t(w), tw0);
                     if (c.trace && tile_id >= 0 && !cur.dup && cur.nb == 0) {  // first n-block's observation
                         const RecvTile rt = c.recv[cur.mine];
                         trace_seen(c, PERSEUS_EV_DISPATCH_SEEN, rt.src, tile_id,
@@ -375,24 +377,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
     } else if (warp < 4 || warp >= 8) {
         // ---------------- copy warps: dispatch puts ----------------
-        // Two queues started at t=0: self tiles (local copy; the GEMM consumes
-        // them first) and remote tiles (NVLink, dst-interleaved).  Warps 2-3
-        // drain the self queue first, warps 8-11 the remote queue first.
+        // Copy warps first copy the self tiles of the head pairs (the GEMMs start
+        // on them), then stream the remote tiles (NVLink, rotated destination
+        // order), then the rest of the self tiles.
         const int remote_units = hdr.n_send_remote * kUnitsPerTile;
         const int self_units = (hdr.n_send - hdr.n_send_remote) * kUnitsPerTile;
+        const int head_units = min(self_units, 2 * hdr.self_head * kUnitsPerTile);
         const uint64_t tc0 = globaltimer();
-        bool remote_q = warp >= 8;
-        bool other_done = false, first_remote = true;
+        // warps 10-11 open the remote stream at once (the first destination's
+        // group must land while the head computes)
+        int state = (head_units > 0 && warp < 10) ? 0 : 1;  // 0: self head, 1: remote, 2: self rest
+        bool first_remote = true;
         while (true) {
+            const bool remote_q = state == 1;
             int u = 0;
             if (lane == 0) u = int(atomicAdd(&c.sched[remote_q ? 1 : 2], 1u));
             u = __shfl_sync(0xffffffffu, u, 0);
             if (u >= (remote_q ? remote_units : self_units)) {
-                if (other_done) break;
-                other_done = true;
-                remote_q = !remote_q;
+                if (state == 2) break;
+                state = state == 0 ? 1 : 2;
                 continue;
             }
+            if (state == 0 && u >= head_units) state = 1;  // head claimed: this unit, then the remote queue
             if (!remote_q) {
                 // Pace the self copies: stay at most kSelfWindow tiles ahead of the
                 // tiles the scheduler has handed out, so heap rows are still in L2
@@ -425,7 +431,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (lane == 0) done = atom_add_acq_rel_gpu(c.send_done + sp, uint32_t(nrows)) + nrows == uint32_t(st.rows);
             if (!__shfl_sync(0xffffffffu, done, 0)) continue;
             if (st.dst == c.rank) {
-                if (lane == 0) st_release_gpu(c.self_ready + st.recv_pos, c.epoch);
+                if (lane == 0) {
+                    st_release_gpu(c.self_ready + st.recv_pos, c.epoch);
+                    if (c.trace) trace_ev(c, kEvDiagSelfReady, c.rank, st.recv_pos, -1, 0, 0, fwd_now());
+                }
                 continue;
             }
             if (lane == 0) {
@@ -635,7 +644,12 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     f.n2 = c.H / 256;
     f.kb1 = c.H / kBK;
     f.kb2 = c.I / kBK;
-    f.lag = std::max(1, (grid + f.n1 - 1) / f.n1);  // pairs: half as many concurrent items
+    // GEMM2 of pair t is issued with GEMM1 of pair t + lag: one wave of the
+    // grid/2 CTA pairs of GEMM1 items in between, so its inputs are normally done
+    {
+        static const int lag_pairs = [] { const char* e = getenv("PERSEUS_LAG_PAIRS"); return e ? atoi(e) : 0; }();
+        f.lag = lag_pairs > 0 ? lag_pairs : std::max(1, (grid / 2 + f.n1 - 1) / f.n1);
+    }
     f.pf = prefetch_cfg();
     f.smaps = smaps;
     f.a1_row_base = a1_row_base;

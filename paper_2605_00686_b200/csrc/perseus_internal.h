@@ -83,7 +83,7 @@ struct PlanHeader {
     int32_t total_tiles;    // reference tile ids in use (all PEs)
     int32_t error;
     int32_t n_pairs;        // M-tile pairs (same expert) for the CTA-pair kernel
-    int32_t pad;
+    int32_t self_head;      // self pairs processed before the remote ones
     int64_t remote_rows_in; // rows received from peers (heap rows before the self segment)
 };
 
@@ -129,6 +129,11 @@ struct TraceEv {
     uint32_t aux;     // signals: 1 = first flag after the group's fence; observes: 1 = content complete when seen
     uint32_t pad;
 };
+
+// diagnostic event kinds (trace mode; ignored by perseus_trace_analyze):
+//   self tile copied (tile = recv position), GEMM1 item dependency wait
+//   (tile = recv position, group = n-block, bytes = ns waited, aux = item index)
+constexpr int kEvDiagSelfReady = 20, kEvDiagItemWait = 21;
 
 // Per-forward communication timestamps (globaltimer ns), reset by the plan
 // kernel and folded into the stats by the combine kernel's last CTA.

@@ -304,7 +304,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         h.total_tiles = s_total_tiles;
         h.error = s_err;
         h.n_pairs = n_pairs;
-        h.pad = 0;
+        h.self_head = s_head;
         h.remote_rows_in = rows_in_r;
         *c.hdr = h;
         if (s_err) atomicAdd(&c.stats[kStatErrors], 1ull);
