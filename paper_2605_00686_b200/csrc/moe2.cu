@@ -78,22 +78,34 @@ __device__ __forceinline__ Item item_of(int w, int T, const Args& f) {
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 __device__ __forceinline__ void copy_unit(const DevCtx& c, const SendTile& st, int r0, int nrows, int lane) {
+    // both rows' loads in flight before any store: one memory latency per unit
     const int32_t abs0 = c.offsets[st.expert] + st.row0 + r0;
     bf16* dbase = c.heap[st.dst] + (size_t(c.par) * c.R_max + st.heap_row + r0) * c.H;
     const int nvec = c.H / 8;
-    for (int rr = 0; rr < nrows; ++rr) {
-        const int32_t tok = c.rows[abs0 + rr];
-        const uint4* src = reinterpret_cast<const uint4*>(c.x + size_t(tok) * c.H);
-        uint4* dst = reinterpret_cast<uint4*>(dbase + size_t(rr) * c.H);
-        int v = lane;
-        for (; v + 224 < nvec; v += 256) {
-            uint4 a[8];
+    const int32_t tok0 = c.rows[abs0];
+    const int32_t tok1 = nrows > 1 ? c.rows[abs0 + 1] : tok0;
+    const uint4* s0 = reinterpret_cast<const uint4*>(c.x + size_t(tok0) * c.H);
+    const uint4* s1 = reinterpret_cast<const uint4*>(c.x + size_t(tok1) * c.H);
+    uint4* d0 = reinterpret_cast<uint4*>(dbase);
+    uint4* d1 = reinterpret_cast<uint4*>(dbase + c.H);
+    int v = lane;
+    for (; v + 224 < nvec; v += 256) {
+        uint4 a[8], b[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) a[u] = __ldg(src + v + 32 * u);
+        for (int u = 0; u < 8; ++u) a[u] = __ldg(s0 + v + 32 * u);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) dst[v + 32 * u] = a[u];
+        for (int u = 0; u < 8; ++u) b[u] = __ldg(s1 + v + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d0[v + 32 * u] = a[u];
+        if (nrows > 1) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) d1[v + 32 * u] = b[u];
         }
-        for (; v < nvec; v += 32) dst[v] = __ldg(src + v);
+    }
+    for (; v < nvec; v += 32) {
+        const uint4 a = __ldg(s0 + v), b = __ldg(s1 + v);
+        d0[v] = a;
+        if (nrows > 1) d1[v] = b;
     }
 }
 
