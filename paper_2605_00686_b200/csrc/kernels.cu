@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "layer_dev.h"
 #include "perseus.h"
@@ -381,15 +382,20 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
 // One CTA per token, one thread per 16-byte column chunk.  Only the (at most
 // k) combine tiles that carry this token's rows are waited on — the tile of
 // sorted slot p is send tile send_first[e] + (p - offsets[e]) / 128.
-template <int K>
+template <int K, int CPT>
 __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
+    // TPC tokens per CTA, TT = H / (8 * CPT) threads per token, CPT 16-byte
+    // column chunks per thread (all CPT * k loads in flight)
     pdl_wait();
     tl_start(c, kTlCombine);
-    const int t = blockIdx.x, v = threadIdx.x;
+    const int TT = c.H / (8 * CPT);
+    const int tl = threadIdx.x / TT, v = threadIdx.x - tl * TT;
+    const int t = blockIdx.x * (blockDim.x / TT) + tl;
     const int k = K > 0 ? K : c.k;
+    const bool live = t < c.S;
     uint64_t t_start = 0;
-    if (c.P > 1 && v == 0) t_start = fwd_now();
-    if (c.P > 1 && v < k) {
+    if (c.P > 1 && threadIdx.x == 0) t_start = fwd_now();
+    if (c.P > 1 && live && v < k) {
         const int e = c.ids[size_t(t) * k + v];
         if (e % c.P != c.rank) {
             const int32_t rel = c.pos[size_t(t) * k + v] - c.offsets[e];
@@ -405,10 +411,12 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
         }
     }
     __syncthreads();
-    if (c.P > 1 && v == 0) {
+    if (c.P > 1 && threadIdx.x == 0) {
         // exposed-communication accounting: the longest any CTA waited for its
         // combine flags; the last CTA folds this forward's timestamps into the stats
-        atomicMax(c.fwd_t + kFwdWaitMax, fwd_now() - t_start);
+        const unsigned long long waited = fwd_now() - t_start;
+        if (waited > *reinterpret_cast<volatile unsigned long long*>(c.fwd_t + kFwdWaitMax))
+            atomicMax(c.fwd_t + kFwdWaitMax, waited);
         __threadfence();
         if (atomicAdd(c.fwd_t + kFwdDoneCtas, 1ull) == gridDim.x - 1) {
             __threadfence();
@@ -419,34 +427,40 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
             atomicAdd(&c.stats[kStatCombineWaitNs], ft[kFwdWaitMax]);
         }
     }
+    if (!live) return;
     const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
     constexpr int KM = K > 0 ? K : 16;
-    uint4 u[KM];
+    uint4 u[CPT][KM];
     float w[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
         if (j < k) {
             const int32_t p = c.pos[size_t(t) * k + j];
             w[j] = c.weights[size_t(t) * k + j];
-            u[j] = *reinterpret_cast<const uint4*>(y + size_t(p) * c.H + v * 8);
+#pragma unroll
+            for (int q = 0; q < CPT; ++q)
+                u[q][j] = *reinterpret_cast<const uint4*>(y + size_t(p) * c.H + (v + q * TT) * 8);
         }
     }
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int j = 0; j < KM; ++j) {
-        if (j < k) {
-            const bf16* b = reinterpret_cast<const bf16*>(&u[j]);
+    for (int q = 0; q < CPT; ++q) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] = __fmaf_rn(w[j], __bfloat162float(b[q]), acc[q]);
+        for (int j = 0; j < KM; ++j) {
+            if (j < k) {
+                const bf16* b = reinterpret_cast<const bf16*>(&u[q][j]);
+#pragma unroll
+                for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(w[j], __bfloat162float(b[z]), acc[z]);
+            }
         }
+        uint4 o;
+        o.x = pack_bf16(acc[0], acc[1]);
+        o.y = pack_bf16(acc[2], acc[3]);
+        o.z = pack_bf16(acc[4], acc[5]);
+        o.w = pack_bf16(acc[6], acc[7]);
+        *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + (v + q * TT) * 8) = o;
     }
-    uint4 o;
-    o.x = pack_bf16(acc[0], acc[1]);
-    o.y = pack_bf16(acc[2], acc[3]);
-    o.z = pack_bf16(acc[4], acc[5]);
-    o.w = pack_bf16(acc[6], acc[7]);
-    *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + v * 8) = o;
-    tl_end(c, kTlCombine, v == 0);
+    tl_end(c, kTlCombine, threadIdx.x == 0);
 }
 
 // ------------------------------------------------------------- launchers ----
@@ -487,15 +501,31 @@ void launch_plan(const DevCtx& c, cudaStream_t st) {
 
 void launch_dispatch(const DevCtx& c, cudaStream_t st) { k_dispatch<<<c.max_send, 256, 0, st>>>(c); }
 
-void launch_combine(const DevCtx& c, cudaStream_t st) {
-    const int threads = c.H / 8;  // H <= 8192
+// combine variant: chunks per thread (1: one token per CTA; 2: two tokens per
+// 256-thread CTA at H = 2048), PERSEUS_COMBINE_CPT overrides (experiments)
+static int combine_cpt(const DevCtx& c) {
+    static const int env = [] { const char* e = getenv("PERSEUS_COMBINE_CPT"); return e ? atoi(e) : 0; }();
+    const int cpt = env > 0 ? env : 2;
+    return (c.H % (8 * cpt) == 0 && c.H / (8 * cpt) <= 1024) ? cpt : 1;
+}
+
+template <int CPT>
+static void launch_combine_cpt(const DevCtx& c, cudaStream_t st) {
+    const int tt = c.H / (8 * CPT);                 // threads per token
+    const int tpc = std::max(1, 256 / tt);          // tokens per CTA
+    const dim3 grid((c.S + tpc - 1) / tpc), block(tt * tpc);
     switch (c.k) {
-        case 1: launch_pdl(k_combine<1>, dim3(c.S), dim3(threads), 0, st, c); break;
-        case 2: launch_pdl(k_combine<2>, dim3(c.S), dim3(threads), 0, st, c); break;
-        case 4: launch_pdl(k_combine<4>, dim3(c.S), dim3(threads), 0, st, c); break;
-        case 8: launch_pdl(k_combine<8>, dim3(c.S), dim3(threads), 0, st, c); break;
-        default: launch_pdl(k_combine<0>, dim3(c.S), dim3(threads), 0, st, c); break;
+        case 1: launch_pdl(k_combine<1, CPT>, grid, block, 0, st, c); break;
+        case 2: launch_pdl(k_combine<2, CPT>, grid, block, 0, st, c); break;
+        case 4: launch_pdl(k_combine<4, CPT>, grid, block, 0, st, c); break;
+        case 8: launch_pdl(k_combine<8, CPT>, grid, block, 0, st, c); break;
+        default: launch_pdl(k_combine<0, CPT>, grid, block, 0, st, c); break;
     }
+}
+
+void launch_combine(const DevCtx& c, cudaStream_t st) {
+    if (combine_cpt(c) == 2) launch_combine_cpt<2>(c, st);
+    else launch_combine_cpt<1>(c, st);
 }
 
 // Every kernel of the forward asks for the maximum shared-memory carveout, so
@@ -514,9 +544,10 @@ cudaError_t configure_kernels(const DevCtx& c) {
                              int(std::max(perm_smem_bytes(c), plan_smem_bytes(c))));
     if (e != cudaSuccess) return e;
     const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_perm), max_carveout(k_plan4), max_carveout(k_dispatch),
-                              max_carveout(k_gate), max_carveout(k_synth_fill), max_carveout(k_combine<0>),
-                              max_carveout(k_combine<1>), max_carveout(k_combine<2>), max_carveout(k_combine<4>),
-                              max_carveout(k_combine<8>)};
+                              max_carveout(k_gate), max_carveout(k_synth_fill), max_carveout(k_combine<0, 1>),
+                              max_carveout(k_combine<1, 1>), max_carveout(k_combine<2, 1>), max_carveout(k_combine<4, 1>),
+                              max_carveout(k_combine<8, 1>), max_carveout(k_combine<0, 2>), max_carveout(k_combine<1, 2>),
+                              max_carveout(k_combine<2, 2>), max_carveout(k_combine<4, 2>), max_carveout(k_combine<8, 2>)};
     for (cudaError_t x : es)
         if (x != cudaSuccess) return x;
     return cudaSuccess;
