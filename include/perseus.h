@@ -234,8 +234,10 @@ int perseus_layer_read_count_table(perseus_layer* layer, int32_t* table);
 
 /* Kernel timeline of every following forward (diagnostics): globaltimer ns
  * [start, end] per kernel in the order router GEMM, route, permute, plan,
- * fused kernel, combine, dispatch, GEMM1, GEMM2 (0 = did not run).  Start =
- * first CTAs after their dependency wait, end = last CTAs. */
+ * fused kernel, combine, dispatch, GEMM1, GEMM2 (0 = did not run), then three
+ * fused-kernel events as [first, last] over its CTAs: MMA issuer out of work
+ * items, copy warps done, epilogue done.  Kernel start = first CTAs after their
+ * dependency wait, end = last CTAs. */
 int perseus_layer_set_timeline(perseus_layer* layer, int on);
 int perseus_layer_read_timeline(perseus_layer* layer, uint64_t* start_end, int n_kernels);
 

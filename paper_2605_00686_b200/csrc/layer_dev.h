@@ -83,7 +83,7 @@ struct DevCtx {
 
 // kernel ids of the diagnostic timeline (DevCtx::tl)
 enum TlKernel : int { kTlGate = 0, kTlRoute, kTlPerm, kTlPlan, kTlFused, kTlCombine, kTlDispatch, kTlGemm1, kTlGemm2,
-                      kTlCount };
+                      kTlMmaOut, kTlCopyEnd, kTlEpiEnd, kTlCount };
 
 #ifdef __CUDACC__
 // Launch with programmatic stream serialization (the kernel calls pdl_wait()

@@ -383,6 +383,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
             }
             atomicAdd(&c.stats[kStatMmaCycles], (unsigned long long)(clock64() - cy0));
+            if (c.tl) {  // when the first / last MMA issuer ran out of work items
+                atomicMax(c.tl + 2 * kTlMmaOut, ~fwd_now());
+                atomicMax(c.tl + 2 * kTlMmaOut + 1, fwd_now());
+            }
             atomicAdd(&c.stats[kStatMmaRingWait], (unsigned long long)cy_ring);
             atomicAdd(&c.stats[kStatMmaAccWait], (unsigned long long)cy_acc);
             atomicAdd(&c.stats[kStatMmaDataWait], (unsigned long long)cy_data);
@@ -464,6 +468,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (lane == 0) atomicMax(c.fwd_t + kFwdDispLast, fwd_now());
         }
         if (lane == 0) atomicAdd(&c.stats[kStatCopyNs], (unsigned long long)(globaltimer() - tc0));
+        if (c.tl && lane == 0) {
+            atomicMax(c.tl + 2 * kTlCopyEnd, ~fwd_now());
+            atomicMax(c.tl + 2 * kTlCopyEnd + 1, fwd_now());
+        }
         // the routing weights (router GEMM ran on a side stream), after the puts
         if (c.weights_late) {
             const int cw = warp < 4 ? warp - 2 : warp - 6;  // 0..5

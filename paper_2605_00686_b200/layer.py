@@ -164,7 +164,8 @@ class MoELayer:
         """Record per-stage CUDA events in the following forwards (off by default)."""
         check(lib.perseus_layer_set_stage_timing(self._h, int(bool(on))))
 
-    TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2")
+    TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2",
+                        "mma_out_of_work", "copy_warps_done", "epilogue_done")
 
     def set_trace(self, on: bool = True) -> None:
         """Device event log of every following forward (puts, fences, flag writes,
