@@ -668,7 +668,12 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     // grid/2 CTA pairs of GEMM1 items in between, so its inputs are normally done
     {
         static const int lag_pairs = [] { const char* e = getenv("PERSEUS_LAG_PAIRS"); return e ? atoi(e) : 0; }();
-        f.lag = lag_pairs > 0 ? lag_pairs : std::max(1, (grid / 2 + f.n1 - 1) / f.n1);
+        const int pairs_live = grid / 2;
+        int lag = std::max(1, (pairs_live + f.n1 - 1) / f.n1);
+        // GEMM2 items longer than GEMM1 items (Llama4: K = 8192 vs 5120): keep two
+        // waves of GEMM2 items for the end, or the last wave runs half empty
+        if (f.kb2 > f.kb1) lag = std::max(lag, (2 * pairs_live + f.n2 - 1) / f.n2);
+        f.lag = lag_pairs > 0 ? lag_pairs : lag;
     }
     f.pf = prefetch_cfg();
     f.smaps = smaps;
