@@ -219,6 +219,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="perseus", choices=["perseus", "reference"])
     ap.add_argument("--config", default="qwen3", choices=list(CONFIGS))
+    ap.add_argument("--experts", type=int, default=0,
+                    help="profiling only: override the expert count (e.g. E/4 at EP=1 = one GPU's share at EP=4)")
     ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU (S)")
     ap.add_argument("--signaling", default="combined", choices=["combined", "vanilla", "decoupled"])
     ap.add_argument("--group-size", type=int, default=0, help="decoupled signal group size (0 = per destination PE)")
@@ -268,7 +270,9 @@ def main():
 
     import paper_2605_00686_b200 as pb
 
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.experts:
+        cfg["E"] = args.experts
     H, I, E, k, S = cfg["H"], cfg["I"], cfg["E"], cfg["k"], args.tokens
     model = pb.ModelConfig(args.config, H, I, E, k)
     proto = {"combined": pb.combined_protocol(args.group_size), "vanilla": pb.vanilla_protocol(),

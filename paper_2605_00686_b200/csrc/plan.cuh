@@ -66,16 +66,16 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     int32_t* off = hr + PE;     // sorted offset per (s, e)
     int32_t* sp = off + PE;     // send position per (kd, j)
     int32_t* rp = sp + E;       // recv position per (ks, j)
-    int32_t* pp = rp + E;       // pair position per (ks, j)
+    int32_t* pp = rp + E;       // pair position per (class, j): class = arrival index of a pair's later tile
     int32_t* selfo = pp + E;    // [El] self-segment row offsets
     __shared__ int32_t s_err, s_total_tiles, s_rows_in, s_n_send, s_n_recv, s_n_pairs;
     __shared__ int32_t dst_first[kMaxPes], dst_n[kMaxPes], dst_group[kMaxPes], n_dgroups;
     __shared__ int32_t src_first[kMaxPes], src_n[kMaxPes], src_group[kMaxPes], n_cgroups_pe;
-    __shared__ int32_t src_pfirst[kMaxPes], src_np[kMaxPes];
+    __shared__ int32_t cls_first[kMaxPes], cls_n[kMaxPes];
     // rotated schedules: sender r streams destination r+1, r+2, ... in turn, so
     // receiver r gets source r-1, r-2, ... one at a time (one group completes
     // after another instead of all at the end)
-    __shared__ int32_t send_base[kMaxPes], recv_base[kMaxPes], recv_pbase[kMaxPes], s_head;
+    __shared__ int32_t send_base[kMaxPes], recv_base[kMaxPes], s_head;
 
     if (tid == 0) s_err = 0;
     if (tid < P && !wait_flag_geq(c.count_flag[r] + tid, c.epoch, kWaitTimeoutNs)) {
@@ -121,14 +121,29 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         // receive key order: self first, then remote sources ascending
         for (int s = 0; s < P; ++s) {
             const int ks = s == r ? 0 : (s < r ? s + 1 : s);
-            for (int j = lane; j < El; j += 32) {
-                const int32_t nt = ceil_tiles(T[s * E + r + P * j]);
-                rp[ks * El + j] = nt;
-                pp[ks * El + j] = (nt + 1) / 2;
+            for (int j = lane; j < El; j += 32) rp[ks * El + j] = ceil_tiles(T[s * E + r + P * j]);
+        }
+        // M-tile pairs per local expert over its tiles in ARRIVAL order (self,
+        // then sources r-1, r-2, ...): a pair may join tiles of two sources, so
+        // one-tile segments (DeepSeek-V3: 128 rows per (source, expert)) still
+        // fill both CTAs of a pair.  A pair's class = the arrival index of its
+        // later tile; pp[class][j] = pairs of expert j in that class
+        for (int j = lane; j < El; j += 32) {
+            int n_all = 0;
+            for (int a = 0; a < P; ++a) n_all += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
+            for (int a = 0; a < P; ++a) pp[a * El + j] = 0;
+            int a = 0, lim = ceil_tiles(T[r * E + r + P * j]);  // list positions [0, lim) come from class a
+            for (int m = 0; 2 * m < n_all; ++m) {
+                const int last = min(2 * m + 1, n_all - 1);
+                while (last >= lim) {
+                    ++a;
+                    lim += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
+                }
+                ++pp[a * El + j];
             }
         }
         const int32_t n_recv = warp_scan(rp, E);
-        const int32_t n_pairs = warp_scan(pp, E);
+        const int32_t n_pairs = warp_scan(pp, E);  // class-major pair positions
         if (lane == 0) {
             s_n_send = n_send;
             s_n_recv = n_recv;
@@ -150,25 +165,24 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 src_first[s] = first;
                 src_n[s] = last - first;
                 src_group[s] = (s != r && last > first) ? g++ : -1;
-                const int pf = pp[ks * El], pl = ks + 1 < P ? pp[(ks + 1) * El] : n_pairs;
-                src_pfirst[s] = pf;
-                src_np[s] = pl - pf;
+            }
+            for (int a = 0; a < P; ++a) {
+                cls_first[a] = pp[a * El];
+                cls_n[a] = (a + 1 < P ? pp[(a + 1) * El] : n_pairs) - cls_first[a];
             }
             n_cgroups_pe = g;
-            int sb = 0, rb = 0, pb = 0;
+            int sb = 0, rb = 0;
             for (int i = 1; i < P; ++i) {
                 const int dd = (r + i) % P, ss = (r - i + P) % P;
                 send_base[dd] = sb;
                 sb += dst_n[dd];
                 recv_base[ss] = rb;
                 rb += src_n[ss];
-                recv_pbase[ss] = pb;
-                pb += src_np[ss];
             }
             // self pairs ahead of the remote ones: enough to cover the arrival of
             // the first source's first signal group (host-estimated link time per
             // tile / compute time per pair), at least ~two waves of GEMM1 items
-            const int n_self_p = src_np[r];
+            const int n_self_p = cls_n[0];  // pairs of self tiles only
             int head = n_self_p;
             if (P > 1) {
                 const int fs = (r - 1 + P) % P;
@@ -264,18 +278,42 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 // source by source in arrival order
                 c.rorder[s == r ? p : n_recv_self + recv_base[s] + (p - src_first[s])] = p;
             }
-            // M-tile pairs (consecutive chunks of one segment; odd tail paired with -1)
-            // in processing order: a head of self pairs (work while the first
-            // remote group is in flight), the remote pairs source by source in
-            // arrival order (their outputs travel back, so they finish early),
-            // then the rest of the self pairs — the tail needs no NVLink round trip
-            const int n_rem_p = n_pairs - src_np[r], head = s_head;
-            for (int pi = 0; 2 * pi < nt; ++pi) {
-                const int q = pp[ks * El + j] + pi;
-                const int po = s == r ? (q < head ? q : q + n_rem_p) : head + recv_pbase[s] + (q - src_pfirst[s]);
+        }
+        // M-tile pairs in processing order: a head of self-only pairs (work while
+        // the first remote group is in flight), the pairs with remote tiles class
+        // by class = source by source in arrival order (their outputs travel
+        // back, so they finish early), then the rest of the self-only pairs — the
+        // tail needs no NVLink round trip
+        const int n0 = cls_n[0], head = s_head;
+        for (int j = t2; j < El; j += 64) {
+            int n_all = 0;
+            for (int a = 0; a < P; ++a) n_all += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
+            // recv position of list position li of expert j (arrival order)
+            auto tile_at = [&](int li) {
+                for (int a = 0; a < P; ++a) {
+                    const int s = (r - a + P) % P;
+                    const int nt = ceil_tiles(T[s * E + r + P * j]);
+                    if (li < nt) {
+                        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+                        return rp[ks * El + j] + li;
+                    }
+                    li -= nt;
+                }
+                return -1;
+            };
+            int a = 0, lim = ceil_tiles(T[r * E + r + P * j]), in_cls = 0;
+            for (int m = 0; 2 * m < n_all; ++m) {
+                const int last = min(2 * m + 1, n_all - 1);
+                while (last >= lim) {
+                    ++a;
+                    lim += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
+                    in_cls = 0;
+                }
+                const int q = pp[a * El + j] + in_cls++;
+                const int po = a == 0 ? (q < head ? q : q + (n_pairs - n0)) : head + (q - n0);
                 if (po < c.max_recv) {
-                    c.pairs[2 * po] = pos0 + 2 * pi;
-                    c.pairs[2 * po + 1] = 2 * pi + 1 < nt ? pos0 + 2 * pi + 1 : -1;
+                    c.pairs[2 * po] = tile_at(2 * m);
+                    c.pairs[2 * po + 1] = 2 * m + 1 < n_all ? tile_at(2 * m + 1) : -1;
                 }
             }
         }
