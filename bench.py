@@ -279,9 +279,10 @@ def main():
              "decoupled": pb.decoupled_protocol(args.group_size)}[args.signaling]
     layer = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing,
                         skew=args.skew, seed=1, protocol=proto, fused=not args.unfused,
-                        pair=not args.no_pair)
+                        pair=False if args.no_pair else None)
     if world > 1:
         layer.connect_dist()
+    layer_info = layer.info()
     stream = torch.cuda.current_stream()
     x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
     out = torch.empty_like(x)
@@ -380,7 +381,7 @@ def main():
     variant = None
     if world > 1 and args.variant_steps > 0 and args.signaling != "vanilla":
         vl = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing, skew=args.skew,
-                         seed=1, protocol=pb.vanilla_protocol(), fused=not args.unfused, pair=not args.no_pair)
+                         seed=1, protocol=pb.vanilla_protocol(), fused=not args.unfused, pair=False if args.no_pair else None)
         vl.connect_dist()
         for _ in range(args.warmup):
             vl.forward(x, out)
@@ -413,8 +414,8 @@ def main():
     tflops_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     if not args.unfused:
-        kname = "k_moe2 (fused dispatch + GEMM1/SwiGLU + GEMM2/combine-put, tcgen05 cta_group::2)" if not args.no_pair \
-            else "k_moe (fused, tcgen05 cta_group::1)"
+        kname = "k_moe2 (fused dispatch + GEMM1/SwiGLU + GEMM2/combine-put, tcgen05 cta_group::2)" \
+            if layer_info["cta_pairs"] else "k_moe (fused, tcgen05 cta_group::1)"
         k_ms = st_mean[2]
         k_flop = 6.0 * H * I * rows
         k_bytes = (E // world) * 3.0 * H * I * 2 + 2.0 * rows * H * 2 + 2.0 * rows * I * 2 + rows * H * 2.0
@@ -467,7 +468,7 @@ def main():
         # and copy-warp busy fraction (per CTA: 2 copy warps)
         dc["frac_wait_dispatch"] = dc["wait_dispatch_ns"] / dc["cta_ns"]
         dc["frac_wait_g1"] = dc["wait_g1_ns"] / dc["cta_ns"]
-        dc["frac_copy_busy"] = dc["copy_ns"] / ((6 if not args.no_pair else 2) * dc["cta_ns"])
+        dc["frac_copy_busy"] = dc["copy_ns"] / ((6 if layer_info["cta_pairs"] else 2) * dc["cta_ns"])
     if dc.get("mma_cycles"):
         # MMA issuer (leader CTA of each pair): where the tensor pipe's feeder waits
         for key in ("mma_ring_wait", "mma_acc_wait", "mma_data_wait"):
@@ -518,7 +519,7 @@ def main():
                                  st_mean)),
             "timeline_us": timeline_us,
             "fused": not args.unfused,
-            "cta_pairs": not args.no_pair and not args.unfused,
+            "cta_pairs": layer_info["cta_pairs"],
             "group_size": args.group_size,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes, "hbm_bytes": hbm_layer,

@@ -127,6 +127,7 @@ typedef struct perseus_layer_config {
 #define PERSEUS_F_SYNTH_WEIGHTS 1 /* generate weights on device from `seed` */
 #define PERSEUS_F_UNFUSED 2       /* forward() as stream-ordered stage kernels instead of the fused persistent kernel */
 #define PERSEUS_F_NO_PAIR 4       /* fused kernel on single CTAs (cta_group::1) instead of CTA pairs (cta_group::2) */
+#define PERSEUS_F_FORCE_PAIR 8    /* CTA pairs even when local experts get at most one 128-row tile */
 
 /* Tile granularity: 128 token rows per transfer tile / GEMM M-tile, i.e. the
  * reference's tile_bytes = 128 * H * 2 (workload.hpp:58). */
@@ -245,6 +246,12 @@ int perseus_layer_read_timeline(perseus_layer* layer, uint64_t* start_end, int n
  * t = alpha + beta * bytes over n >= 2 points (ConfigError if degenerate). */
 int perseus_fit_alpha_beta(const double* bytes, const double* ns, size_t n, double* alpha_ns,
                            double* beta_ns_per_byte, double* r_squared);
+
+/* Which forward path the layer runs: fused persistent kernel or stage kernels;
+ * CTA-pair (cta_group::2) tiles or 1-CTA tiles (chosen at create: pairs unless
+ * PERSEUS_F_NO_PAIR, or each local expert gets at most one 128-row tile and
+ * PERSEUS_F_FORCE_PAIR is not set). */
+int perseus_layer_info(perseus_layer* layer, int* fused, int* cta_pairs);
 
 /* ---- device event log (trace mode) -> the reference's RunTrace ----------
  * With tracing on, every forward records what the kernels actually did:

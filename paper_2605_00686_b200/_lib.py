@@ -18,6 +18,7 @@ PHASE_ROUTE, PHASE_DISPATCH, PHASE_EXPERT, PHASE_COMBINE, PHASE_ALL = 0, 1, 2, 3
 F_SYNTH_WEIGHTS = 1
 F_UNFUSED = 2
 F_NO_PAIR = 4
+F_FORCE_PAIR = 8
 TILE_ROWS = 128
 
 
@@ -123,6 +124,7 @@ def _load():
         "perseus_layer_set_stage_timing": (C.c_int, [vp, C.c_int]),
         "perseus_layer_set_timeline": (C.c_int, [vp, C.c_int]),
         "perseus_layer_set_trace": (C.c_int, [vp, C.c_int]),
+        "perseus_layer_info": (C.c_int, [vp, P(C.c_int), P(C.c_int)]),
         "perseus_layer_read_trace": (C.c_int, [vp, P(TraceEvent), sz, P(sz)]),
         "perseus_fit_alpha_beta": (C.c_int, [P(C.c_double), P(C.c_double), sz, P(C.c_double), P(C.c_double),
                                             P(C.c_double)]),

@@ -379,7 +379,13 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
         try {
             L->cfg = *cfg;
             L->fused = !(cfg->flags & PERSEUS_F_UNFUSED);
-            L->pair = !(cfg->flags & PERSEUS_F_NO_PAIR);
+            // CTA pairs share one expert's weights across two 128-row tiles; when a
+            // local expert receives at most one tile per forward on average
+            // (DeepSeek-V3 at EP=1: 128 rows) the second CTA of every pair would
+            // idle, so the 1-CTA fused kernel is used instead
+            L->pair = !(cfg->flags & PERSEUS_F_NO_PAIR) &&
+                      ((cfg->flags & PERSEUS_F_FORCE_PAIR) ||
+                       int64_t(world) * int64_t(cfg->tokens_per_pe) * cfg->top_k > int64_t(kTileRows) * cfg->experts);
             L->rank = rank;
             L->world = world;
             L->device = device;
@@ -742,6 +748,13 @@ int perseus_layer_read_timeline(perseus_layer* L, uint64_t* start_end, int n) {
             start_end[2 * i] = h[2 * i] ? ~h[2 * i] : 0;
             start_end[2 * i + 1] = h[2 * i + 1];
         }
+    });
+}
+
+int perseus_layer_info(perseus_layer* L, int* fused, int* cta_pairs) {
+    return guarded([&] {
+        if (fused) *fused = L->fused ? 1 : 0;
+        if (cta_pairs) *cta_pairs = (L->fused && L->pair) ? 1 : 0;
     });
 }
 

@@ -41,7 +41,7 @@ class MoELayer:
     def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
                  device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
                  protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True,
-                 fused: bool = True, pair: bool = True):
+                 fused: bool = True, pair: Optional[bool] = None):
         protocol = protocol or combined_protocol(0)
         self.fused = fused
         self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
@@ -50,7 +50,8 @@ class MoELayer:
                                tokens_per_pe, ROUTING[routing], float(skew), seed,
                                protocol.device_signaling(), protocol.group_size,
                                (_lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
-                               | (0 if fused else _lib.F_UNFUSED) | (0 if pair else _lib.F_NO_PAIR))
+                               | (0 if fused else _lib.F_UNFUSED)
+                               | {None: 0, True: _lib.F_FORCE_PAIR, False: _lib.F_NO_PAIR}[pair])
         self._cfg = cfg
         h = C.c_void_p()
         check(lib.perseus_layer_create(C.byref(cfg), rank, world, device, C.byref(h)))
@@ -166,6 +167,12 @@ class MoELayer:
 
     TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2",
                         "mma_out_of_work", "copy_warps_done", "epilogue_done")
+
+    def info(self) -> dict:
+        """The forward path chosen at create: fused kernel, CTA-pair tiles."""
+        fused, pairs = C.c_int(), C.c_int()
+        check(lib.perseus_layer_info(self._h, C.byref(fused), C.byref(pairs)))
+        return {"fused": bool(fused.value), "cta_pairs": bool(pairs.value)}
 
     def set_trace(self, on: bool = True) -> None:
         """Device event log of every following forward (puts, fences, flag writes,

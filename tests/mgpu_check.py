@@ -43,7 +43,7 @@ def main():
     for routing, skew, proto, H, I, E, k, S in cases:
         m = pb.ModelConfig("m", H, I, E, k)
         layer = pb.MoELayer(m, S, rank=rank, world=world, device=local, routing=routing, skew=skew,
-                            seed=7, protocol=proto)
+                            seed=7, protocol=proto, pair=True)  # the CTA-pair kernel even at small S
         layer.connect_dist()
         x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
         out = torch.empty_like(x)
@@ -91,7 +91,8 @@ def main():
                   pb.ProtocolConfig(signaling="decoupled", ordering="nic_fence", suppress_fences=True),
                   pb.ProtocolConfig(signaling="coupled", suppress_fences=True)):
         m = pb.ModelConfig("m", H, I, E, k)
-        layer = pb.MoELayer(m, S, rank=rank, world=world, device=local, routing="balanced", seed=3, protocol=proto)
+        layer = pb.MoELayer(m, S, rank=rank, world=world, device=local, routing="balanced", seed=3, protocol=proto,
+                            pair=True)
         layer.connect_dist()
         x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
         out = torch.empty_like(x)

@@ -197,7 +197,7 @@ def test_other_baseline_shapes_single_gpu(oracle, preset, S, routing):
     from tests.gpu_util import shape_of
     pb = _pb()
     m = pb.model_preset(preset)
-    l = pb.MoELayer(m, S, routing=routing, seed=4)
+    l = pb.MoELayer(m, S, routing=routing, seed=4, pair=True)
     x = torch.empty(S, m.hidden_dim, dtype=torch.bfloat16, device="cuda")
     l.fill_synthetic_x(x, 4)
     out = torch.empty_like(x)
