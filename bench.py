@@ -358,9 +358,13 @@ def main():
         barrier()
         return allmax(time.perf_counter() - t0)
 
+    enqueue = []
+
     def run_async(n):
+        t0 = time.perf_counter()
         for _ in range(n):
             layer.forward_host_async(xh, oh)
+        enqueue.append((time.perf_counter() - t0) / n)
         layer.host_wait()
 
     def run_sync(n):
@@ -534,6 +538,7 @@ def main():
                     "d2h_bytes_per_step": S * H * 2, "ms_per_step": 1e3 * te_async / args.steps,
                     "api": "perseus_layer_forward_host_async (pinned host buffers, copies pipelined across steps)",
                     "output_matches_device_forward": e2e_ok,
+                    "host_enqueue_ms_per_step": 1e3 * enqueue[-1],
                     "blocking_api": {"value": e2e_sync_value, "unit": "tokens/s",
                                      "api": "perseus_layer_forward_host (copy in, forward, copy out, sync per call)"}},
             "gpu_launches": launches_per_step * args.steps,
