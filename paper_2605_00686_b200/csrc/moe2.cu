@@ -53,7 +53,7 @@ constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 
 struct Args {
     int32_t n1, n2, kb1, kb2, lag;
-    int32_t pf;  // L2 prefetch: distance in k-blocks (bits 0-7), operands (bit 8: A, bit 9: B)
+    int32_t pad0;
     const CUtensorMap* smaps;  // store maps, box 64 x 32, SW128: [0] hbuf, [1 + p] ybuf of PE p
     int64_t a1_row_base;
 };
@@ -223,8 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (lane == 0) {
             // ---------------- scheduler (leader) + TMA producer (both) ----------------
             // One item of lookahead: the next item is taken a few k-blocks before
-            // the current one ends (optionally, operand k-blocks are prefetched
-            // into L2 that many blocks ahead of their TMA load, f.pf).
+            // the current one ends.
             unsigned long long wait_d = 0, wait_g = 0, wait_r = 0;
             int stage = 0, slot = 0;
             uint32_t phase = 0, rphase = 0;
@@ -276,11 +275,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 }
                 return o;
             };
-            const int pf_dist = f.pf & 0xff;
-            auto prefetch = [&](const Op& o, int kb) {
-                if (f.pf & 0x100) tma_prefetch_l2_2d(o.ta, kb * kBK, o.a_row);
-                if (f.pf & 0x200) tma_prefetch_l2_2d(o.tb, kb * kBK, o.b_row);
-            };
             int w = grab();
             Op cur{};
             if (w >= 0) cur = op_of(w);
@@ -310,16 +304,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 fence_proxy_async();
                 int wn = -2;  // not taken yet
                 Op nxt{};
-                const int take_at = max(0, cur.nkb - max(pf_dist, 1));
+                const int take_at = max(0, cur.nkb - 1);
                 for (int kb = 0; kb < cur.nkb; ++kb) {
                     if (kb == take_at) {
                         wn = grab();
                         if (wn >= 0) nxt = op_of(wn);
-                    }
-                    if (pf_dist > 0) {
-                        const int pk = kb + pf_dist;
-                        if (pk < cur.nkb) prefetch(cur, pk);
-                        else if (wn >= 0 && pk - cur.nkb < nxt.nkb) prefetch(nxt, pk - cur.nkb);
                     }
                     uint8_t* sa = smem + stage * kStage;
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -508,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             RecvTile rt;
             if (mine >= 0) rt = c.recv[mine];
             const bool valid = mine >= 0 && row < rt.rows;
-            const bool full_tile = mine >= 0 && rt.rows == kTileRows && !(f.pf & 0x400);
+            const bool full_tile = mine >= 0 && rt.rows == kTileRows;
             if (it.kind == 1) {
                 if (full_tile) {
                     // h = silu(gate) * up -> hbuf via TMA tensor stores
@@ -638,21 +627,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 
-// L2 prefetch of operand boxes ahead of their TMA loads; PERSEUS_PREFETCH="<dist>[,a][,b]"
-// overrides the default (experiments)
-static int prefetch_cfg() {
-    static int cfg = [] {
-        const char* e = getenv("PERSEUS_PREFETCH");
-        if (!e) return 0;
-        int dist = atoi(e), bits = 0;
-        if (strchr(e, 'a')) bits |= 0x100;
-        if (strchr(e, 'b')) bits |= 0x200;
-        if (strchr(e, 'd')) bits |= 0x400;  // epilogue: direct stores instead of TMA tensor stores
-        return (dist & 0xff) | bits;
-    }();
-    return cfg;
-}
-
 cudaError_t configure_moe2() {
     return cudaFuncSetAttribute(k_moe2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
 }
@@ -675,7 +649,7 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
         if (f.kb2 > f.kb1) lag = std::max(lag, (2 * pairs_live + f.n2 - 1) / f.n2);
         f.lag = lag_pairs > 0 ? lag_pairs : lag;
     }
-    f.pf = prefetch_cfg();
+    f.pad0 = 0;
     f.smaps = smaps;
     f.a1_row_base = a1_row_base;
     DevCtx cc = c;

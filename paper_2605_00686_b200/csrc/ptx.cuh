@@ -59,12 +59,6 @@ DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
 DEVI void tma_prefetch_desc(const void* desc) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
 }
-// L2 prefetch of one 2D box of a tensor map (no smem, no completion)
-DEVI void tma_prefetch_l2_2d(const void* desc, int32_t c0, int32_t c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(desc)),
-                 "r"(c0), "r"(c1)
-                 : "memory");
-}
 // 2D tiled load global -> shared, completes `bytes` on `bar`.  c0 = inner (K)
 // coordinate in elements, c1 = row.
 DEVI void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0, int32_t c1) {
