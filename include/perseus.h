@@ -308,6 +308,10 @@ typedef struct perseus_trace_report {
  * combine direction mirrors them (same tiles, reversed). */
 int perseus_trace_analyze(const perseus_trace_event* events, size_t n, int nic_ordering,
                           const perseus_transfer* transfers, size_t n_transfers, perseus_trace_report* out);
+/* The same RunTrace of one direction (0 dispatch, 1 combine) in the reference's text
+ * format (sigsim::serialize_trace, trace.cpp:33-51); call with buf = NULL to size. */
+int perseus_trace_serialize(const perseus_trace_event* events, size_t n, int nic_ordering, int direction,
+                            char* buf, size_t cap, size_t* len);
 
 /* Record per-stage CUDA events in every following forward (off by default: each
  * event record costs stream time). */

@@ -128,6 +128,7 @@ def _load():
         "perseus_layer_read_trace": (C.c_int, [vp, P(TraceEvent), sz, P(sz)]),
         "perseus_fit_alpha_beta": (C.c_int, [P(C.c_double), P(C.c_double), sz, P(C.c_double), P(C.c_double),
                                             P(C.c_double)]),
+        "perseus_trace_serialize": (C.c_int, [P(TraceEvent), sz, C.c_int, C.c_int, C.c_char_p, sz, P(sz)]),
         "perseus_trace_analyze": (C.c_int, [P(TraceEvent), sz, C.c_int, P(Transfer), sz, P(TraceReport)]),
         "perseus_layer_read_timeline": (C.c_int, [vp, P(C.c_uint64), C.c_int]),
     }

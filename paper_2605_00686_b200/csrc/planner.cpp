@@ -513,84 +513,119 @@ uint64_t perseus_heap_digest(const uint64_t* ext, size_t n_ext, const uint64_t* 
     return h;
 }
 
+}  // extern "C"
+
+namespace {
+// One direction's device events (all PEs) as a sigsim::RunTrace (see perseus.h):
+// puts -> Submit/Put; group fences -> Submit/FenceMarker (ProxyFence) or the flag on
+// the group's first signal (NicFence); flag writes -> NicServiceStart/Signal;
+// receiver observations -> SignalVisible + Completion/Put at the time the tile's
+// content was first complete.
+sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int dir, bool nic_ordering,
+                                  int64_t* late_tiles) {
+    const int base = dir == 0 ? PERSEUS_EV_DISPATCH_PUT : PERSEUS_EV_COMBINE_PUT;
+    sigsim::RunTrace tr;
+    std::map<int64_t, uint64_t> put_bytes;  // tile -> bytes
+    for (size_t i = 0; i < n; ++i)
+        if (ev[i].kind == base) put_bytes[ev[i].tile] = ev[i].bytes;
+    for (size_t i = 0; i < n; ++i) {
+        const perseus_trace_event& e = ev[i];
+        const int k = e.kind - base;
+        if (k < 0 || k > 3) continue;
+        sigsim::TraceRecord r;
+        r.time = sigsim::TimeNs(e.t);
+        r.pe = uint32_t(e.pe);
+        r.tile_id = e.tile;
+        r.group_id = e.group;
+        if (k == 0) {
+            r.kind = sigsim::TraceKind::Submit;
+            r.req_kind = sigsim::ReqKind::Put;
+            r.src_pe = uint32_t(e.pe);
+            r.dst_pe = uint32_t(e.peer);
+            r.size = e.bytes;
+            tr.total_put_bytes_submitted += e.bytes;
+            tr.add(r);
+        } else if (k == 1) {
+            if (nic_ordering) continue;
+            r.kind = sigsim::TraceKind::Submit;
+            r.req_kind = sigsim::ReqKind::FenceMarker;
+            r.src_pe = uint32_t(e.pe);
+            r.dst_pe = uint32_t(e.peer);
+            tr.add(r);
+        } else if (k == 2) {
+            r.kind = sigsim::TraceKind::NicServiceStart;
+            r.req_kind = sigsim::ReqKind::Signal;
+            r.src_pe = uint32_t(e.pe);
+            r.dst_pe = uint32_t(e.peer);
+            r.fence_flag = nic_ordering && e.aux != 0;
+            tr.add(r);
+        } else {
+            r.kind = sigsim::TraceKind::SignalVisible;
+            r.req_kind = sigsim::ReqKind::Signal;
+            r.src_pe = uint32_t(e.peer);
+            r.dst_pe = uint32_t(e.pe);
+            tr.add(r);
+            sigsim::TraceRecord c = r;
+            c.kind = sigsim::TraceKind::Completion;
+            c.req_kind = sigsim::ReqKind::Put;
+            c.time = sigsim::TimeNs(e.t + (e.aux ? 0 : e.bytes));
+            auto it = put_bytes.find(e.tile);
+            c.size = it == put_bytes.end() ? 0 : it->second;
+            tr.total_put_bytes_delivered += c.size;
+            tr.add(c);
+            if (!e.aux && late_tiles) ++*late_tiles;
+        }
+    }
+    std::stable_sort(tr.records.begin(), tr.records.end(),
+                     [](const sigsim::TraceRecord& a, const sigsim::TraceRecord& b) { return a.time < b.time; });
+    if (!tr.records.empty()) tr.makespan = tr.records.back().time - tr.records.front().time;
+    return tr;
+}
+
+sigsim::DispatchWorkload realised_workload(const perseus_transfer* transfers, size_t n, int dir) {
+    sigsim::DispatchWorkload wl;
+    for (size_t i = 0; i < n; ++i) {
+        sigsim::TransferSpec t = from_c(transfers[i]);
+        if (dir == 1) std::swap(t.src_pe, t.dst_pe);  // combine: the same tiles travelling back
+        wl.remote_transfers.push_back(t);
+    }
+    return wl;
+}
+}  // namespace
+
+extern "C" {
+
 int perseus_trace_analyze(const perseus_trace_event* ev, size_t n, int nic_ordering,
                           const perseus_transfer* transfers, size_t n_transfers, perseus_trace_report* out) {
     return guarded([&] {
         *out = perseus_trace_report{};
         for (int dir = 0; dir < 2; ++dir) {
-            const int base = dir == 0 ? PERSEUS_EV_DISPATCH_PUT : PERSEUS_EV_COMBINE_PUT;
-            sigsim::RunTrace tr;
-            std::map<int64_t, uint64_t> put_bytes;  // tile -> bytes
-            for (size_t i = 0; i < n; ++i)
-                if (ev[i].kind == base) put_bytes[ev[i].tile] = ev[i].bytes;
-            for (size_t i = 0; i < n; ++i) {
-                const perseus_trace_event& e = ev[i];
-                const int k = e.kind - base;
-                if (k < 0 || k > 3) continue;
-                sigsim::TraceRecord r;
-                r.time = sigsim::TimeNs(e.t);
-                r.pe = uint32_t(e.pe);
-                r.tile_id = e.tile;
-                r.group_id = e.group;
-                if (k == 0) {  // put issued by its sender
-                    r.kind = sigsim::TraceKind::Submit;
-                    r.req_kind = sigsim::ReqKind::Put;
-                    r.src_pe = uint32_t(e.pe);
-                    r.dst_pe = uint32_t(e.peer);
-                    r.size = e.bytes;
-                    tr.total_put_bytes_submitted += e.bytes;
-                    tr.add(r);
-                } else if (k == 1) {  // a group's fence: a fence marker unless the protocol orders at the NIC
-                    if (nic_ordering) continue;
-                    r.kind = sigsim::TraceKind::Submit;
-                    r.req_kind = sigsim::ReqKind::FenceMarker;
-                    r.src_pe = uint32_t(e.pe);
-                    r.dst_pe = uint32_t(e.peer);
-                    tr.add(r);
-                } else if (k == 2) {  // flag word written (the first after a fence carries it for NicFence)
-                    r.kind = sigsim::TraceKind::NicServiceStart;
-                    r.req_kind = sigsim::ReqKind::Signal;
-                    r.src_pe = uint32_t(e.pe);
-                    r.dst_pe = uint32_t(e.peer);
-                    r.fence_flag = nic_ordering && e.aux != 0;
-                    tr.add(r);
-                } else {  // receiver: signal visible; data landed when its content was first complete
-                    r.kind = sigsim::TraceKind::SignalVisible;
-                    r.req_kind = sigsim::ReqKind::Signal;
-                    r.src_pe = uint32_t(e.peer);
-                    r.dst_pe = uint32_t(e.pe);
-                    tr.add(r);
-                    sigsim::TraceRecord c = r;
-                    c.kind = sigsim::TraceKind::Completion;
-                    c.req_kind = sigsim::ReqKind::Put;
-                    c.time = sigsim::TimeNs(e.t + (e.aux ? 0 : e.bytes));
-                    auto it = put_bytes.find(e.tile);
-                    c.size = it == put_bytes.end() ? 0 : it->second;
-                    tr.total_put_bytes_delivered += c.size;
-                    tr.add(c);
-                    if (!e.aux) ++out->late_tiles[dir];
-                }
-            }
-            std::stable_sort(tr.records.begin(), tr.records.end(),
-                             [](const sigsim::TraceRecord& a, const sigsim::TraceRecord& b) { return a.time < b.time; });
+            const sigsim::RunTrace tr = device_run_trace(ev, n, dir, nic_ordering != 0, &out->late_tiles[dir]);
             const auto acc = sigsim::fence_accounting(tr);
             out->records += int64_t(tr.records.size());
             out->fence_count[dir] = acc.fence_count;
             out->flagged_signal_count[dir] = acc.flagged_signal_count;
             out->ordering_violations[dir] = int64_t(sigsim::verify_ordering(tr).size());
             out->put_bytes[dir] = int64_t(tr.total_put_bytes_submitted);
-            // the realised transfers (combine: the same tiles travelling back)
-            sigsim::DispatchWorkload wl;
-            for (size_t i = 0; i < n_transfers; ++i) {
-                sigsim::TransferSpec t = from_c(transfers[i]);
-                if (dir == 1) std::swap(t.src_pe, t.dst_pe);
-                wl.remote_transfers.push_back(t);
-            }
-            const auto rep = sigsim::conservation_check(tr, wl);
+            const auto rep = sigsim::conservation_check(tr, realised_workload(transfers, n_transfers, dir));
             out->conservation_ok[dir] = rep.pass ? 1 : 0;
             if (!rep.pass && !out->conservation_error[0] && !rep.failures.empty())
                 std::snprintf(out->conservation_error, sizeof out->conservation_error, "%s: %s",
                               dir == 0 ? "dispatch" : "combine", rep.failures.front().c_str());
+        }
+    });
+}
+
+int perseus_trace_serialize(const perseus_trace_event* ev, size_t n, int nic_ordering, int direction,
+                            char* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        if (direction != 0 && direction != 1) throw sigsim::ConfigError("direction must be 0 (dispatch) or 1 (combine)");
+        const std::string text = sigsim::serialize_trace(device_run_trace(ev, n, direction, nic_ordering != 0, nullptr));
+        *len = text.size();
+        if (buf && cap) {
+            const size_t m = std::min(cap - 1, text.size());
+            std::memcpy(buf, text.data(), m);
+            buf[m] = 0;
         }
     });
 }

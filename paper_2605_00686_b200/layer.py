@@ -238,3 +238,16 @@ def analyze_trace(events: np.ndarray, protocol: ProtocolConfig, transfers: np.nd
     rep = _lib.TraceReport()
     check(lib.perseus_trace_analyze(ebuf, n, int(protocol.ordering == "nic_fence"), tbuf, len(tr), C.byref(rep)))
     return rep.as_dict()
+
+
+def serialize_trace(events: np.ndarray, protocol: ProtocolConfig, direction: int = 0) -> str:
+    """One direction's device RunTrace in the reference's text format (sigsim::serialize_trace)."""
+    ev = np.ascontiguousarray(events)
+    n = len(ev)
+    ebuf = (_lib.TraceEvent * max(1, n)).from_buffer_copy(ev.tobytes() or bytes(C.sizeof(_lib.TraceEvent)))
+    ln = C.c_size_t(0)
+    nic = int(protocol.ordering == "nic_fence")
+    check(lib.perseus_trace_serialize(ebuf, n, nic, direction, None, 0, C.byref(ln)))
+    buf = C.create_string_buffer(ln.value + 1)
+    check(lib.perseus_trace_serialize(ebuf, n, nic, direction, buf, ln.value + 1, C.byref(ln)))
+    return buf.value.decode()

@@ -133,3 +133,19 @@ def test_two_rank_trace_adapter_flags_a_tile_signalled_twice(results):
     assert not rep["dispatch"]["conservation_ok"], rep
     err = rep["conservation_error"]
     assert "2 times" in err or "delivered bytes" in err, err
+
+
+def test_device_trace_serializes_in_the_reference_format(results):
+    """perseus_trace_serialize: the device RunTrace in sigsim::serialize_trace's text
+    format (trace.cpp:33-51): header line, one record per line."""
+    proto = pb.vanilla_protocol()
+    wl = pb.build_dispatch(MODEL, pb.ClusterConfig(P, 1, 1), S, 1.0, 128 * MODEL.hidden_dim * 2, 5)
+    ev = np.concatenate([_events_for_rank(r, wl, proto) for r in range(P)])
+    text = pb.serialize_trace(ev, proto, 0)
+    lines = text.strip().splitlines()
+    assert lines[0].startswith("# trace v1 ")
+    kinds = [ln.split()[2] for ln in lines[1:]]
+    n_fence = sum(1 for ln in lines[1:] if ln.split()[3] == "fence")
+    assert n_fence == results["vanilla"][1]
+    assert len(lines) - 1 == len([e for e in ev if e["kind"] in (1, 2, 3)]) + 2 * len([e for e in ev if e["kind"] == 4])
+    assert set(kinds) <= {"submit", "nic_service_start", "signal_visible", "completion"}, set(kinds)
