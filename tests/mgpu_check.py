@@ -111,6 +111,13 @@ def main():
             dist.all_gather_object(tr, layer.layout()[0])
             if rank == 0:
                 reps.append(pb.analyze_trace(np.concatenate(ev), proto, np.concatenate(tr)))
+                if len(reps) == 1 and not proto.suppress_fences:
+                    # one real forward's device RunTrace in the reference's text format
+                    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+                    name = f"device_trace_{proto.mode_name()}_p{world}"
+                    for d, tag in ((0, "dispatch"), (1, "combine")):
+                        with open(os.path.join(ROOT, "gpurun_out", f"{name}_{tag}.txt"), "w") as fh:
+                            fh.write(pb.serialize_trace(np.concatenate(ev), proto, d))
         layer.set_trace(False)
         layer.close()
         dist.barrier()
