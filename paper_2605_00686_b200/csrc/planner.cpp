@@ -525,6 +525,13 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
                                   int64_t* late_tiles) {
     const int base = dir == 0 ? PERSEUS_EV_DISPATCH_PUT : PERSEUS_EV_COMBINE_PUT;
     sigsim::RunTrace tr;
+    // each PE stamps its own globaltimer: times are made relative to the PE's first
+    // event of the forward (ordering checks compare times recorded on one PE only)
+    std::map<int32_t, uint64_t> t0;
+    for (size_t i = 0; i < n; ++i) {
+        auto it = t0.find(ev[i].pe);
+        if (it == t0.end() || ev[i].t < it->second) t0[ev[i].pe] = ev[i].t;
+    }
     std::map<int64_t, uint64_t> put_bytes;  // tile -> bytes
     for (size_t i = 0; i < n; ++i)
         if (ev[i].kind == base) put_bytes[ev[i].tile] = ev[i].bytes;
@@ -533,7 +540,7 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
         const int k = e.kind - base;
         if (k < 0 || k > 3) continue;
         sigsim::TraceRecord r;
-        r.time = sigsim::TimeNs(e.t);
+        r.time = sigsim::TimeNs(e.t - t0[e.pe]);
         r.pe = uint32_t(e.pe);
         r.tile_id = e.tile;
         r.group_id = e.group;
@@ -568,7 +575,7 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
             sigsim::TraceRecord c = r;
             c.kind = sigsim::TraceKind::Completion;
             c.req_kind = sigsim::ReqKind::Put;
-            c.time = sigsim::TimeNs(e.t + (e.aux ? 0 : e.bytes));
+            c.time = sigsim::TimeNs(e.t - t0[e.pe] + (e.aux ? 0 : e.bytes));
             auto it = put_bytes.find(e.tile);
             c.size = it == put_bytes.end() ? 0 : it->second;
             tr.total_put_bytes_delivered += c.size;
