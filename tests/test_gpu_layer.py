@@ -274,3 +274,28 @@ def test_device_trace_to_reference_runtrace(oracle, P, proto):
     assert got == want, (got, want)
     for l in layers:
         l.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("S,routing,pair", [(1000, "gate", True), (777, "zipf", None), (777, "gate", False)])
+def test_fused_forward_ragged_token_counts(oracle, S, routing, pair):
+    """Token counts that are not multiples of the 8-token route blocks, the 256-token
+    permutation blocks or the combine's 2-token CTAs, through the fused forward
+    (CTA-pair and 1-CTA kernels): routing bit-exact, output vs the oracle on a subset."""
+    import torch
+    from tests.gpu_util import shape_of
+    pb = _pb()
+    m = pb.model_preset("qwen3-30b")
+    l = pb.MoELayer(m, S, routing=routing, skew=1.3, seed=6, pair=pair)
+    x = torch.empty(S, m.hidden_dim, dtype=torch.bfloat16, device="cuda")
+    out = torch.zeros_like(x)
+    l.fill_synthetic_x(x, 6)
+    for _ in range(2):
+        l.forward(x, out)
+    torch.cuda.synchronize()
+    c = l.counters()
+    assert c["wait_timeouts"] == 0 and c["errors"] == 0, c
+    subset = np.sort(np.concatenate([np.random.default_rng(1).choice(S - 8, 24, replace=False),
+                                     np.arange(S - 8, S)]))  # incl. the ragged tail
+    _check_rank(oracle, pb, shape_of(m, S, 1), l, x, out, routing, 6, 1.3, 0, subset=subset)
+    l.close()
