@@ -5,6 +5,8 @@ Bars (north_star): routing ids, token permutation, per-destination tile /
 fence counts, tile ids and heap offsets bit-exact; layer output within bf16
 tolerance (max-abs and normwise relative error <= 1e-2 vs the fp32 oracle).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -299,3 +301,22 @@ def test_fused_forward_ragged_token_counts(oracle, S, routing, pair):
                                      np.arange(S - 8, S)]))  # incl. the ragged tail
     _check_rank(oracle, pb, shape_of(m, S, 1), l, x, out, routing, 6, 1.3, 0, subset=subset)
     l.close()
+
+
+@pytest.mark.gpu
+def test_c_abi_only_program(tmp_path):
+    """A plain C program using only include/perseus.h (no Python, no torch) runs the
+    layer end to end on the GPU: blocking and pipelined host APIs agree bit for bit."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "layer_c_abi")
+    libdir = os.path.join(root, "paper_2605_00686_b200")
+    subprocess.run(["gcc", "-std=c11", "-O1", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "layer_c_abi.c"), "-L", libdir, "-lperseus",
+                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "layer_c_abi: pass" in r.stdout
