@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(256, 1)
 // the dispatch puts, GEMM1+SwiGLU and GEMM2+combine-put of a forward with
 // tile-granular dependencies instead of kernel boundaries:
 //   warps 2-3 (copy warps): stream 16-row units of the send tiles, in the
-//     dst-interleaved copy order, into the destination heaps (NVLink stores
+//     rotated destination order, into the destination heaps (NVLink stores
 //     for peers); the warp completing a tile runs Perseus Phase 1/2, or marks
 //     a self tile ready (gpu-scope release).
 //   warp 0 (scheduler + TMA producer): grabs work items from a global atomic

@@ -326,7 +326,7 @@ __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33
 
 __device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 
-// (The per-forward plan is in plan.cu.)
+// (The per-forward plan is in plan.cuh, run by k_perm's extra CTA.)
 
 // -------------------------------------------------------------- dispatch ----
 // One CTA per send tile: gather the tile's token rows (sorted order) and store

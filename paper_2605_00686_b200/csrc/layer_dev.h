@@ -59,8 +59,8 @@ struct DevCtx {
     uint32_t* cgroup_ctr;
     uint32_t* tile_ctr;
     int32_t max_send, max_recv;
-    // fused-kernel scheduling (rebuilt by k_plan every forward)
-    int32_t* sorder;      // [max_send]: send positions in copy order (dst-interleaved)
+    // fused-kernel scheduling (rebuilt by the plan every forward)
+    int32_t* sorder;      // [max_send]: remote send positions in copy order (rotated destinations)
     int32_t* rorder;      // [max_recv]: recv positions in processing order (self, then by arrival)
     uint32_t* send_done;  // [max_send]: rows copied per send tile
     uint32_t* g1_done;    // [max_recv]: GEMM1 n-blocks finished per M-tile

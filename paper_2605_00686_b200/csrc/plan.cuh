@@ -181,7 +181,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             }
             // self pairs ahead of the remote ones: enough to cover the arrival of
             // the first source's first signal group (host-estimated link time per
-            // tile / compute time per pair), at least ~two waves of GEMM1 items
+            // tile / compute time per pair), at least one wave of GEMM1 items
             const int n_self_p = cls_n[0];  // pairs of self tiles only
             int head = n_self_p;
             if (P > 1) {
