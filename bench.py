@@ -460,6 +460,9 @@ def main():
         nvl_src = "profiles/r01_nvlink_p2p_bw.json (measured SM peer stores)"
     t_roof = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / nvl_bw, hbm_layer / (hbm_peak * 1e9))
     layer_frac = t_roof / (ms_step / 1e3)
+    # north_star's figure: the slower of compute-at-peak and bytes-over-NVLink (no HBM term)
+    t_cn = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / nvl_bw)
+    frac_cn = t_cn / (ms_step / 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -526,6 +529,7 @@ def main():
             "cta_pairs": layer_info["cta_pairs"],
             "group_size": args.group_size,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
+                               "frac_of_max_compute_nvlink": frac_cn,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes, "hbm_bytes": hbm_layer,
                                "t_tensor_us": flops_layer / (tflops_peak * 1e12) * 1e6,
                                "t_nvlink_us": nvl_bytes / nvl_bw * 1e6, "nvlink_gbs": nvl_bw / 1e9,
