@@ -521,7 +521,9 @@ namespace {
 // the group's first signal (NicFence); flag writes -> NicServiceStart/Signal;
 // receiver observations -> SignalVisible + Completion/Put at the time the tile's
 // content was first complete.
-sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int dir, bool nic_ordering,
+// ordering: 0 ProxyFence (fences -> FenceMarker records), 1 NicFence (the group's first
+// flag carries the fence), 2 GPU-direct (the reference records neither, protocols.cpp:244-246)
+sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int dir, int ordering,
                                   int64_t* late_tiles) {
     const int base = dir == 0 ? PERSEUS_EV_DISPATCH_PUT : PERSEUS_EV_COMBINE_PUT;
     sigsim::RunTrace tr;
@@ -553,7 +555,7 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
             tr.total_put_bytes_submitted += e.bytes;
             tr.add(r);
         } else if (k == 1) {
-            if (nic_ordering) continue;
+            if (ordering != 0) continue;
             r.kind = sigsim::TraceKind::Submit;
             r.req_kind = sigsim::ReqKind::FenceMarker;
             r.src_pe = uint32_t(e.pe);
@@ -564,7 +566,7 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
             r.req_kind = sigsim::ReqKind::Signal;
             r.src_pe = uint32_t(e.pe);
             r.dst_pe = uint32_t(e.peer);
-            r.fence_flag = nic_ordering && e.aux != 0;
+            r.fence_flag = ordering == 1 && e.aux != 0;
             tr.add(r);
         } else {
             r.kind = sigsim::TraceKind::SignalVisible;
@@ -607,7 +609,7 @@ int perseus_trace_analyze(const perseus_trace_event* ev, size_t n, int nic_order
     return guarded([&] {
         *out = perseus_trace_report{};
         for (int dir = 0; dir < 2; ++dir) {
-            const sigsim::RunTrace tr = device_run_trace(ev, n, dir, nic_ordering != 0, &out->late_tiles[dir]);
+            const sigsim::RunTrace tr = device_run_trace(ev, n, dir, nic_ordering, &out->late_tiles[dir]);
             const auto acc = sigsim::fence_accounting(tr);
             out->records += int64_t(tr.records.size());
             out->fence_count[dir] = acc.fence_count;
@@ -627,7 +629,7 @@ int perseus_trace_serialize(const perseus_trace_event* ev, size_t n, int nic_ord
                             char* buf, size_t cap, size_t* len) {
     return guarded([&] {
         if (direction != 0 && direction != 1) throw sigsim::ConfigError("direction must be 0 (dispatch) or 1 (combine)");
-        const std::string text = sigsim::serialize_trace(device_run_trace(ev, n, direction, nic_ordering != 0, nullptr));
+        const std::string text = sigsim::serialize_trace(device_run_trace(ev, n, direction, nic_ordering, nullptr));
         *len = text.size();
         if (buf && cap) {
             const size_t m = std::min(cap - 1, text.size());

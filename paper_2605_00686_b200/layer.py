@@ -223,6 +223,13 @@ class MoELayer:
             pass
 
 
+def _ordering_mode(protocol: ProtocolConfig) -> int:
+    """0 ProxyFence (fence markers), 1 NicFence (flagged signals), 2 GPU-direct (neither)."""
+    if protocol.transport == "gpu_direct":
+        return 2
+    return 1 if protocol.ordering == "nic_fence" else 0
+
+
 def analyze_trace(events: np.ndarray, protocol: ProtocolConfig, transfers: np.ndarray) -> dict:
     """One forward's device events (all PEs, concatenated) -> sigsim::RunTrace per
     direction -> the reference's fence_accounting / verify_ordering /
@@ -236,7 +243,7 @@ def analyze_trace(events: np.ndarray, protocol: ProtocolConfig, transfers: np.nd
     for i, row in enumerate(tr):
         tbuf[i] = _lib.Transfer(int(row[0]), int(row[1]), int(row[2]), int(row[3]), int(row[4]), int(row[5]))
     rep = _lib.TraceReport()
-    check(lib.perseus_trace_analyze(ebuf, n, int(protocol.ordering == "nic_fence"), tbuf, len(tr), C.byref(rep)))
+    check(lib.perseus_trace_analyze(ebuf, n, _ordering_mode(protocol), tbuf, len(tr), C.byref(rep)))
     return rep.as_dict()
 
 
@@ -246,7 +253,7 @@ def serialize_trace(events: np.ndarray, protocol: ProtocolConfig, direction: int
     n = len(ev)
     ebuf = (_lib.TraceEvent * max(1, n)).from_buffer_copy(ev.tobytes() or bytes(C.sizeof(_lib.TraceEvent)))
     ln = C.c_size_t(0)
-    nic = int(protocol.ordering == "nic_fence")
+    nic = _ordering_mode(protocol)
     check(lib.perseus_trace_serialize(ebuf, n, nic, direction, None, 0, C.byref(ln)))
     buf = C.create_string_buffer(ln.value + 1)
     check(lib.perseus_trace_serialize(ebuf, n, nic, direction, buf, ln.value + 1, C.byref(ln)))

@@ -63,7 +63,7 @@ def _events_for_rank(rank, wl, proto, late_tile=None, dup_signal_tile=None):
     return arr
 
 
-CASES = ["vanilla", "combined", "decoupled_gs2", "late", "dup"]
+CASES = ["vanilla", "combined", "decoupled_gs2", "late", "dup", "gpu_direct"]
 
 
 def _worker(rank, port, q):
@@ -74,7 +74,7 @@ def _worker(rank, port, q):
         for case in CASES:
             proto = {"vanilla": pb.vanilla_protocol(), "combined": pb.combined_protocol(0),
                      "decoupled_gs2": pb.decoupled_protocol(2), "late": pb.combined_protocol(0),
-                     "dup": pb.vanilla_protocol()}[case]
+                     "dup": pb.vanilla_protocol(), "gpu_direct": pb.gpu_direct_protocol()}[case]
             skew = 0.0 if case == "decoupled_gs2" else 1.0  # balanced: gs=2 divides every PE's tile count
             wl = pb.build_dispatch(MODEL, pb.ClusterConfig(P, 1, 1), S, skew, 128 * MODEL.hidden_dim * 2, 5)
             late = wl.remote_transfers[0].tile_id if case == "late" else None
@@ -111,11 +111,13 @@ def results():
     return out
 
 
-@pytest.mark.parametrize("case", ["vanilla", "combined", "decoupled_gs2"])
+@pytest.mark.parametrize("case", ["vanilla", "combined", "decoupled_gs2", "gpu_direct"])
 def test_two_rank_trace_adapter_matches_reference_accounting(results, case):
     rep, want, nbytes = results[case]
     d = rep["dispatch"]
     nic = case == "combined"
+    if case == "gpu_direct":  # the reference records no fence markers and no flagged signals
+        assert want == 0 and d["fence_count"] == 0 and d["flagged_signal_count"] == 0, d
     assert (d["flagged_signal_count"] if nic else d["fence_count"]) == want, (d, want)
     assert (d["fence_count"] if nic else d["flagged_signal_count"]) == 0
     assert d["ordering_violations"] == 0 and d["late_tiles"] == 0
