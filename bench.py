@@ -379,6 +379,25 @@ def main():
     te_async = e2e_run(run_async, args.steps)
     te_sync = e2e_run(run_sync, min(args.steps, 200))
     e2e_value = world * S * args.steps / te_async
+
+    # the copy floor of the same step at the same moment: the upload of x and the
+    # download of out on two streams with no forward (PCIe duplex; on a shared
+    # host this moves between runs, and e2e with it)
+    cp_up, cp_down = torch.cuda.Stream(), torch.cuda.Stream()
+    x_dev2 = torch.empty_like(x)
+
+    def run_copies(n):
+        for _ in range(n):
+            with torch.cuda.stream(cp_up):
+                x_dev2.view(torch.int16).copy_(x_host, non_blocking=True)
+            with torch.cuda.stream(cp_down):
+                o_host.copy_(out.view(torch.int16), non_blocking=True)
+        torch.cuda.synchronize()
+
+    run_copies(3)
+    copy_steps = min(args.steps, 300)
+    te_copy = e2e_run(run_copies, copy_steps)
+    copy_floor_ms = te_copy / copy_steps * 1e3
     e2e_sync_value = world * S * min(args.steps, 200) / te_sync
 
     # ---- the per-tile-fence variant of the same kernel (N > 1) ----
@@ -553,6 +572,8 @@ def main():
                     "d2h_bytes_per_step": S * H * 2, "ms_per_step": 1e3 * te_async / args.steps,
                     "api": "perseus_layer_forward_host_async (pinned host buffers, copies pipelined across steps)",
                     "output_matches_device_forward": e2e_ok,
+                    "copy_floor_ms_per_step": copy_floor_ms,
+                    "copy_floor_note": "H2D of x + D2H of out on two streams, no forward, measured right after",
                     "host_enqueue_ms_per_step": 1e3 * enqueue[-1],
                     "blocking_api": {"value": e2e_sync_value, "unit": "tokens/s",
                                      "api": "perseus_layer_forward_host (copy in, forward, copy out, sync per call)"}},

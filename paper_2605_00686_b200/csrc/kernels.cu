@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         // one sys-scope fence, then the per-source ready flag at every PE
         if (c.P > 1) fence_acq_rel_sys();  // P == 1: the plan kernel is stream-ordered after this one
         for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
+        tl_mark(c, kTlCounts);
     }
     const int32_t total = block_exclusive_scan(tot, E, scratch);
     for (int e = tid; e < E; e += kPermT) {

@@ -83,7 +83,7 @@ struct DevCtx {
 
 // kernel ids of the diagnostic timeline (DevCtx::tl)
 enum TlKernel : int { kTlGate = 0, kTlRoute, kTlPerm, kTlPlan, kTlFused, kTlCombine, kTlDispatch, kTlGemm1, kTlGemm2,
-                      kTlMmaOut, kTlCopyEnd, kTlEpiEnd, kTlCount };
+                      kTlMmaOut, kTlCopyEnd, kTlEpiEnd, kTlCounts, kTlPlanReady, kTlFusedEnter, kTlPlanB, kTlPlanC, kTlCount };
 
 #ifdef __CUDACC__
 // Launch with programmatic stream serialization (the kernel calls pdl_wait()
@@ -117,6 +117,13 @@ __device__ __forceinline__ void tl_start(const DevCtx& c, int id) {
 }
 __device__ __forceinline__ void tl_end(const DevCtx& c, int id, bool me) {
     if (c.tl && me && blockIdx.x + 4 >= gridDim.x) atomicMax(c.tl + 2 * id + 1, fwd_now());
+}
+// a point event (first and last time any caller reached it)
+__device__ __forceinline__ void tl_mark(const DevCtx& c, int id) {
+    if (!c.tl) return;
+    const uint64_t t = fwd_now();
+    atomicMax(c.tl + 2 * id, ~t);
+    atomicMax(c.tl + 2 * id + 1, t);
 }
 
 // Append one event to the device event log (trace mode only).

@@ -53,7 +53,7 @@ constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 
 struct Args {
     int32_t n1, n2, kb1, kb2, lag;
-    int32_t pad0;
+    int32_t lag_end;  // lag over the last pairs (>= lag; see launch_moe2)
     const CUtensorMap* smaps;  // store maps, box 64 x 32, SW128: [0] hbuf, [1 + p] ybuf of PE p
     int64_t a1_row_base;
 };
@@ -62,16 +62,23 @@ struct Item {
 };
 
 __device__ __forceinline__ Item item_of(int w, int T, const Args& f) {
-    const int L = min(f.lag, T), n1 = f.n1, n2 = f.n2;
+    const int L = min(f.lag, T), L2 = max(L, min(f.lag_end, T)), n1 = f.n1, n2 = f.n2;
+    // A: GEMM1 of pairs [0, L)
     if (w < L * n1) return {1, w / n1, w % n1};
     w -= L * n1;
-    const int steady = (T - L) * (n1 + n2);
+    // B: steady state, GEMM1 of pair L + st with GEMM2 of pair st, st in [0, T - L2)
+    const int steady = (T - L2) * (n1 + n2);
     if (w < steady) {
         const int st = w / (n1 + n2), r = w % (n1 + n2);
         return r < n1 ? Item{1, L + st, r} : Item{2, st, r - n1};
     }
     w -= steady;
-    if (w < L * n2) return {2, T - L + w / n2, w % n2};
+    // C: GEMM1 of pairs [T - L2 + L, T): the lag grows to L2 for the end
+    const int c1 = (L2 - L) * n1;
+    if (w < c1) return {1, T - L2 + L + w / n1, w % n1};
+    w -= c1;
+    // D: GEMM2 of pairs [T - L2, T)
+    if (w < L2 * n2) return {2, T - L2 + w / n2, w % n2};
     return {0, 0, 0};
 }
 
@@ -648,8 +655,18 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
         // waves of GEMM2 items for the end, or the last wave runs half empty
         if (f.kb2 > f.kb1) lag = std::max(lag, (2 * pairs_live + f.n2 - 1) / f.n2);
         f.lag = lag_pairs > 0 ? lag_pairs : lag;
+        // the end of the schedule: after the last GEMM1 item is taken, the GEMM2
+        // items still queued must keep every pair busy for that item's duration
+        // (pairs_live * kb1 k-blocks) plus one more wave, or the last pairs' GEMM2
+        // items start late while the others idle (Qwen3 EP=1: 13 -> 35 pairs cut
+        // the MMA tail spread from ~14.5 to ~8.5 us).  Only without remote pairs:
+        // with P > 1 it would hold back the GEMM2 (and combine puts) of the last
+        // remote pairs, exposing their NVLink time (EP=4: 4% -> 12% exposed)
+        static const int lag_end_env = [] { const char* e = getenv("PERSEUS_LAG_END"); return e ? atoi(e) : -1; }();
+        const int cover = (pairs_live * f.kb1 + f.n2 * f.kb2 - 1) / (f.n2 * f.kb2);
+        const int lag_end = c.P == 1 ? std::max(f.lag, cover + (pairs_live + f.n2 - 1) / f.n2) : f.lag;
+        f.lag_end = lag_end_env >= 0 ? std::max(f.lag, lag_end_env) : lag_end;
     }
-    f.pad0 = 0;
     f.smaps = smaps;
     f.a1_row_base = a1_row_base;
     DevCtx cc = c;

@@ -28,11 +28,12 @@ namespace {
 __device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 
 // exclusive scan of a[0..n) in place by ONE warp; returns the total
-__device__ int32_t warp_scan(int32_t* a, int n) {
+__device__ __noinline__ int32_t warp_scan(int32_t* a, int n) {
     __syncwarp();
     const int lane = threadIdx.x & 31;
     const int per = (n + 31) / 32, b = lane * per, e = min(n, b + per);
     int32_t local = 0;
+    #pragma unroll 1
     for (int i = b; i < e; ++i) local += a[i];
     int32_t incl = local;
 #pragma unroll
@@ -41,6 +42,7 @@ __device__ int32_t warp_scan(int32_t* a, int n) {
         if (lane >= o) incl += u;
     }
     int32_t run = incl - local;
+    #pragma unroll 1
     for (int i = b; i < e; ++i) {
         const int32_t v = a[i];
         a[i] = run;
@@ -83,44 +85,60 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         s_err = 1;
     }
     sync128();
+    if (tid == 0) tl_mark(c, kTlPlanReady);
     const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
+    #pragma unroll 1
     for (int i = tid; i < PE; i += 128) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
     if (tid == 0) {
+        #pragma unroll 1
         for (int q = 0; q < 4; ++q) c.sched[q] = 0;
+        #pragma unroll 1
         for (int q = 0; q < kFwdSlots; ++q) c.fwd_t[q] = (q & 1) || q == kFwdDoneCtas ? 0ull : ~0ull;  // min / max
     }
     sync128();
 
     // ---- phase B: four independent scans ----
     if (warp == 0) {
+        #pragma unroll 1
         for (int s = 0; s < P; ++s)
+            #pragma unroll 1
             for (int e = lane; e < E; e += 32) tb[s * E + e] = (s != e % P) ? ceil_tiles(T[s * E + e]) : 0;
         const int32_t tot = warp_scan(tb, PE);
         if (lane == 0) s_total_tiles = tot;
     } else if (warp == 1) {
         // (d, s, j): the rows source s sends to destination d, in the reference's cursor order
+        #pragma unroll 1
         for (int d = 0; d < P; ++d)
+            #pragma unroll 1
             for (int s = 0; s < P; ++s)
+                #pragma unroll 1
                 for (int j = lane; j < El; j += 32) hr[(d * P + s) * El + j] = (s != d) ? T[s * E + d + P * j] : 0;
         const int32_t tot = warp_scan(hr, PE);
         if (lane == 0) s_rows_in = (r + 1 < P ? hr[(r + 1) * P * El] : tot) - hr[r * P * El];
     } else if (warp == 2) {
+        #pragma unroll 1
         for (int s = 0; s < P; ++s) {
+            #pragma unroll 1
             for (int e = lane; e < E; e += 32) off[s * E + e] = T[s * E + e];
             warp_scan(off + s * E, E);
         }
+        #pragma unroll 1
         for (int j = lane; j < El; j += 32) selfo[j] = T[r * E + r + P * j];
         warp_scan(selfo, El);
     } else {
         // send key order: remote destinations ascending, then the self segment
+        #pragma unroll 1
         for (int d = 0; d < P; ++d) {
             const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
+            #pragma unroll 1
             for (int j = lane; j < El; j += 32) sp[kd * El + j] = ceil_tiles(T[r * E + d + P * j]);
         }
         const int32_t n_send = warp_scan(sp, E);
         // receive key order: self first, then remote sources ascending
+        #pragma unroll 1
         for (int s = 0; s < P; ++s) {
             const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+            #pragma unroll 1
             for (int j = lane; j < El; j += 32) rp[ks * El + j] = ceil_tiles(T[s * E + r + P * j]);
         }
         // M-tile pairs per local expert over its tiles in ARRIVAL order (self,
@@ -128,11 +146,15 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         // one-tile segments (DeepSeek-V3: 128 rows per (source, expert)) still
         // fill both CTAs of a pair.  A pair's class = the arrival index of its
         // later tile; pp[class][j] = pairs of expert j in that class
+        #pragma unroll 1
         for (int j = lane; j < El; j += 32) {
             int n_all = 0;
+            #pragma unroll 1
             for (int a = 0; a < P; ++a) n_all += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
+            #pragma unroll 1
             for (int a = 0; a < P; ++a) pp[a * El + j] = 0;
             int a = 0, lim = ceil_tiles(T[r * E + r + P * j]);  // list positions [0, lim) come from class a
+            #pragma unroll 1
             for (int m = 0; 2 * m < n_all; ++m) {
                 const int last = min(2 * m + 1, n_all - 1);
                 while (last >= lim) {
@@ -149,6 +171,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             s_n_recv = n_recv;
             s_n_pairs = n_pairs;
             int g = 0;
+            #pragma unroll 1
             for (int kd = 0; kd < P; ++kd) {
                 const int d = kd < r ? kd : (kd < P - 1 ? kd + 1 : r);
                 const int first = sp[kd * El];
@@ -159,6 +182,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             }
             n_dgroups = g;
             g = 0;
+            #pragma unroll 1
             for (int ks = 0; ks < P; ++ks) {
                 const int s = ks == 0 ? r : (ks <= r ? ks - 1 : ks);
                 const int first = rp[ks * El], last = ks + 1 < P ? rp[(ks + 1) * El] : n_recv;
@@ -166,12 +190,14 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 src_n[s] = last - first;
                 src_group[s] = (s != r && last > first) ? g++ : -1;
             }
+            #pragma unroll 1
             for (int a = 0; a < P; ++a) {
                 cls_first[a] = pp[a * El];
                 cls_n[a] = (a + 1 < P ? pp[(a + 1) * El] : n_pairs) - cls_first[a];
             }
             n_cgroups_pe = g;
             int sb = 0, rb = 0;
+            #pragma unroll 1
             for (int i = 1; i < P; ++i) {
                 const int dd = (r + i) % P, ss = (r - i + P) % P;
                 send_base[dd] = sb;
@@ -193,6 +219,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         }
     }
     sync128();
+    if (tid == 0) tl_mark(c, kTlPlanB);
 
     const int gs = c.group_size;
     const int32_t n_send = s_n_send, n_recv = s_n_recv, n_pairs = s_n_pairs, rows_in_r = s_rows_in;
@@ -206,6 +233,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     // ---- phase C: emit the send side (warps 0-1) and the receive side (warps 2-3) ----
     if (warp < 2) {
         const int t2 = tid;  // 0..63
+        #pragma unroll 1
         for (int e = t2; e < E; e += 64) {
             const int d = e % P, j = e / P;
             const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
@@ -214,6 +242,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             const int32_t pos0 = sp[kd * El + j];
             const int64_t hrow = d != r ? int64_t(hr[(d * P + r) * El + j] - hr[d * P * El]) : int64_t(rows_in_r + selfo[j]);
             c.send_first[e] = pos0;
+            #pragma unroll 1
             for (int ch = 0; ch < nt; ++ch) {
                 const int p = pos0 + ch;
                 if (p >= c.max_send) {
@@ -235,6 +264,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 if (d != r) c.sorder[send_base[d] + (p - dst_first[d])] = p;
             }
         }
+        #pragma unroll 1
         for (int g = t2; g < n_groups; g += 64) {
             Group G;
             if (gs > 0) {
@@ -249,6 +279,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         }
     } else {
         const int t2 = tid - 64;
+        #pragma unroll 1
         for (int i = t2; i < P * El; i += 64) {
             const int s = i / El, j = i - s * El, e = r + P * j;
             const int ks = s == r ? 0 : (s < r ? s + 1 : s);
@@ -256,6 +287,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             const int nt = ceil_tiles(cnt);
             const int32_t pos0 = rp[ks * El + j];
             const int64_t hrow = s != r ? int64_t(hr[(r * P + s) * El + j] - hr[r * P * El]) : int64_t(rows_in_r + selfo[j]);
+            #pragma unroll 1
             for (int ch = 0; ch < nt; ++ch) {
                 const int p = pos0 + ch;
                 if (p >= c.max_recv) {
@@ -285,11 +317,14 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         // back, so they finish early), then the rest of the self-only pairs — the
         // tail needs no NVLink round trip
         const int n0 = cls_n[0], head = s_head;
+        #pragma unroll 1
         for (int j = t2; j < El; j += 64) {
             int n_all = 0;
+            #pragma unroll 1
             for (int a = 0; a < P; ++a) n_all += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
             // recv position of list position li of expert j (arrival order)
             auto tile_at = [&](int li) {
+                #pragma unroll 1
                 for (int a = 0; a < P; ++a) {
                     const int s = (r - a + P) % P;
                     const int nt = ceil_tiles(T[s * E + r + P * j]);
@@ -302,6 +337,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 return -1;
             };
             int a = 0, lim = ceil_tiles(T[r * E + r + P * j]), in_cls = 0;
+            #pragma unroll 1
             for (int m = 0; 2 * m < n_all; ++m) {
                 const int last = min(2 * m + 1, n_all - 1);
                 while (last >= lim) {
@@ -317,6 +353,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 }
             }
         }
+        #pragma unroll 1
         for (int g = t2; g < n_cgroups; g += 64) {
             Group G;
             if (gs > 0) {
@@ -331,6 +368,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         }
     }
     sync128();
+    if (tid == 0) tl_mark(c, kTlPlanC);
     if (tid == 0) {
         PlanHeader h;
         h.n_send = n_send;

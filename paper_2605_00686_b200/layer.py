@@ -166,7 +166,8 @@ class MoELayer:
         check(lib.perseus_layer_set_stage_timing(self._h, int(bool(on))))
 
     TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2",
-                        "mma_out_of_work", "copy_warps_done", "epilogue_done")
+                        "mma_out_of_work", "copy_warps_done", "epilogue_done", "counts_published", "plan_counts_ready",
+                        "fused_cta_entry", "plan_phase_b", "plan_phase_c")
 
     def info(self) -> dict:
         """The forward path chosen at create: fused kernel, CTA-pair tiles."""
