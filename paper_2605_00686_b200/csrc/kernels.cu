@@ -203,11 +203,10 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     if (b == nb) {
         // the plan CTA: waits for every PE's counts (this rank's from CTA 0 below)
         // and builds the plan while the other CTAs rank their tokens
-        if (tid < 128) {
-            if (tid == 0 && c.tl) atomicMax(c.tl + 2 * kTlPlan, ~fwd_now());
-            plan_body(c, sm);
-            if (tid == 0 && c.tl) atomicMax(c.tl + 2 * kTlPlan + 1, fwd_now());
-        }
+        static_assert(kPermT == kPlanThreads, "the plan CTA runs plan_body with all its threads");
+        if (tid == 0 && c.tl) atomicMax(c.tl + 2 * kTlPlan, ~fwd_now());
+        plan_body(c, sm);
+        if (tid == 0 && c.tl) atomicMax(c.tl + 2 * kTlPlan + 1, fwd_now());
         return;
     }
     tl_start(c, kTlPerm);
@@ -471,8 +470,8 @@ void launch_gate_exact(const DevCtx& c, cudaStream_t st) {
     k_gate<<<g, 256, 0, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
 }
 
-// the per-forward plan (plan.cuh), one CTA of 4 warps
-__global__ void __launch_bounds__(128) k_plan4(DevCtx c) {
+// the per-forward plan (plan.cuh), one CTA of 8 warps
+__global__ void __launch_bounds__(kPlanThreads) k_plan4(DevCtx c) {
     pdl_wait();
     pdl_launch_dependents();
     if (c.tl && threadIdx.x == 0) atomicMax(c.tl + 2 * kTlPlan, ~fwd_now());
@@ -497,7 +496,7 @@ size_t perm_smem_bytes(const DevCtx& c) {
 }
 
 void launch_plan(const DevCtx& c, cudaStream_t st) {
-    launch_pdl(k_plan4, dim3(1), dim3(128), plan_smem_bytes(c), st, c);
+    launch_pdl(k_plan4, dim3(1), dim3(kPlanThreads), plan_smem_bytes(c), st, c);
 }
 
 void launch_dispatch(const DevCtx& c, cudaStream_t st) { k_dispatch<<<c.max_send, 256, 0, st>>>(c); }

@@ -190,6 +190,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const bool lead = crank == 0;
 
     if (warp == 0 && lane == 0) {
+        tl_mark(c, kTlFusedEnter);
         tma_prefetch_desc(&tm_a1);
         tma_prefetch_desc(&tm_b1);
         tma_prefetch_desc(&tm_a2);

@@ -25,6 +25,8 @@ using namespace ptx;
 
 namespace {
 
+constexpr int kPlanThreads = 256;  // 8 warps (the permutation kernel's CTA size)
+
 __device__ __forceinline__ int32_t ceil_tiles(int32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 
 // exclusive scan of a[0..n) in place by ONE warp; returns the total
@@ -55,13 +57,13 @@ __device__ __noinline__ int32_t warp_scan(int32_t* a, int n) {
 
 }  // namespace
 
-// The plan, run by threads 0..127 of one CTA (named barrier 1; `sm` holds
-// plan_smem_bytes()).
+// The plan, run by threads 0..kPlanThreads-1 of one CTA (named barrier 1;
+// `sm` holds plan_smem_bytes()).
 __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     const int P = c.P, E = c.E, El = c.E_loc, r = c.rank;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int PE = P * E;
-    auto sync128 = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    auto sync128 = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };  // all kPlanThreads
     int32_t* T = sm;            // [P][E] counts
     int32_t* tb = T + PE;       // tile-id base per (s, e), s-major
     int32_t* hr = tb + PE;      // heap-row scan, (d, s, j) order
@@ -88,7 +90,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     if (tid == 0) tl_mark(c, kTlPlanReady);
     const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
     #pragma unroll 1
-    for (int i = tid; i < PE; i += 128) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
+    for (int i = tid; i < PE; i += kPlanThreads) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
     if (tid == 0) {
         #pragma unroll 1
         for (int q = 0; q < 4; ++q) c.sched[q] = 0;
@@ -122,10 +124,11 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             for (int e = lane; e < E; e += 32) off[s * E + e] = T[s * E + e];
             warp_scan(off + s * E, E);
         }
+    } else if (warp == 6) {
         #pragma unroll 1
         for (int j = lane; j < El; j += 32) selfo[j] = T[r * E + r + P * j];
         warp_scan(selfo, El);
-    } else {
+    } else if (warp == 3) {
         // send key order: remote destinations ascending, then the self segment
         #pragma unroll 1
         for (int d = 0; d < P; ++d) {
@@ -134,6 +137,8 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             for (int j = lane; j < El; j += 32) sp[kd * El + j] = ceil_tiles(T[r * E + d + P * j]);
         }
         const int32_t n_send = warp_scan(sp, E);
+        if (lane == 0) s_n_send = n_send;
+    } else if (warp == 4) {
         // receive key order: self first, then remote sources ascending
         #pragma unroll 1
         for (int s = 0; s < P; ++s) {
@@ -141,6 +146,9 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             #pragma unroll 1
             for (int j = lane; j < El; j += 32) rp[ks * El + j] = ceil_tiles(T[s * E + r + P * j]);
         }
+        const int32_t n_recv = warp_scan(rp, E);
+        if (lane == 0) s_n_recv = n_recv;
+    } else if (warp == 5) {
         // M-tile pairs per local expert over its tiles in ARRIVAL order (self,
         // then sources r-1, r-2, ...): a pair may join tiles of two sources, so
         // one-tile segments (DeepSeek-V3: 128 rows per (source, expert)) still
@@ -164,12 +172,14 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 ++pp[a * El + j];
             }
         }
-        const int32_t n_recv = warp_scan(rp, E);
         const int32_t n_pairs = warp_scan(pp, E);  // class-major pair positions
-        if (lane == 0) {
-            s_n_send = n_send;
-            s_n_recv = n_recv;
-            s_n_pairs = n_pairs;
+        if (lane == 0) s_n_pairs = n_pairs;
+    }
+    sync128();
+    // ---- phase B2: the per-PE group tables (one thread) ----
+    if (tid == 0) {
+        const int32_t n_send = s_n_send, n_recv = s_n_recv, n_pairs = s_n_pairs;
+        {
             int g = 0;
             #pragma unroll 1
             for (int kd = 0; kd < P; ++kd) {
@@ -230,11 +240,12 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     const int32_t n_cgroups = gs > 0 ? n_recv_remote / gs : n_cgroups_pe;
     if (tid == 0 && gs > 0 && (n_send_remote % gs || n_recv_remote % gs)) s_err = 2;
 
-    // ---- phase C: emit the send side (warps 0-1) and the receive side (warps 2-3) ----
-    if (warp < 2) {
-        const int t2 = tid;  // 0..63
+    // ---- phase C: emit the send side (warps 0-3), the receive side (warps 4-5)
+    // and the pair order (warps 6-7) ----
+    if (warp < 4) {
+        const int t2 = tid;  // 0..127
         #pragma unroll 1
-        for (int e = t2; e < E; e += 64) {
+        for (int e = t2; e < E; e += 128) {
             const int d = e % P, j = e / P;
             const int kd = d < r ? d : (d > r ? d - 1 : P - 1);
             const int32_t cnt = T[r * E + e];
@@ -265,7 +276,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             }
         }
         #pragma unroll 1
-        for (int g = t2; g < n_groups; g += 64) {
+        for (int g = t2; g < n_groups; g += 128) {
             Group G;
             if (gs > 0) {
                 G = Group{-1, g * gs, gs, 0};
@@ -277,8 +288,8 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             c.groups[g] = G;
             c.group_ctr[g] = 0;
         }
-    } else {
-        const int t2 = tid - 64;
+    } else if (warp < 6) {
+        const int t2 = tid - 128;  // 0..63
         #pragma unroll 1
         for (int i = t2; i < P * El; i += 64) {
             const int s = i / El, j = i - s * El, e = r + P * j;
@@ -311,6 +322,21 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 c.rorder[s == r ? p : n_recv_self + recv_base[s] + (p - src_first[s])] = p;
             }
         }
+        #pragma unroll 1
+        for (int g = t2; g < n_cgroups; g += 64) {
+            Group G;
+            if (gs > 0) {
+                G = Group{-1, n_recv_self + g * gs, gs, 0};
+            } else {
+                int s = 0;
+                while (src_group[s] != g) ++s;
+                G = Group{s, src_first[s], src_n[s], 0};
+            }
+            c.cgroups[g] = G;
+            c.cgroup_ctr[g] = 0;
+        }
+    } else {
+        const int t2 = tid - 192;  // 0..63
         // M-tile pairs in processing order: a head of self-only pairs (work while
         // the first remote group is in flight), the pairs with remote tiles class
         // by class = source by source in arrival order (their outputs travel
@@ -352,19 +378,6 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                     c.pairs[2 * po + 1] = 2 * m + 1 < n_all ? tile_at(2 * m + 1) : -1;
                 }
             }
-        }
-        #pragma unroll 1
-        for (int g = t2; g < n_cgroups; g += 64) {
-            Group G;
-            if (gs > 0) {
-                G = Group{-1, n_recv_self + g * gs, gs, 0};
-            } else {
-                int s = 0;
-                while (src_group[s] != g) ++s;
-                G = Group{s, src_first[s], src_n[s], 0};
-            }
-            c.cgroups[g] = G;
-            c.cgroup_ctr[g] = 0;
         }
     }
     sync128();
