@@ -469,13 +469,13 @@ def main():
                  "timing": "CUDA events on the layer stream around the kernel, mean of 10 synchronised steps"})
     # the committed ncu capture of the same kernel at this shape (profiles/): its own
     # duration and DRAM bytes — a short, unthrottled run vs the sustained bench clocks
-    ncu_sum = os.path.join(ROOT, "profiles", "r01c_ep1_ncu_summary.json")
+    ncu_sum = os.path.join(ROOT, "profiles", "r01d_ep1_ncu_summary.json")
     if world == 1 and args.config == "qwen3" and not args.unfused and S == 4096 and os.path.exists(ncu_sum):
         with open(ncu_sum) as fh:
             m = json.load(fh)["ncu_full_k_moe2"]
         dur = float(m["metrics"]["gpu__time_duration.sum"][0]) * 1e-6
         nb = float(m["traffic_bytes_per_launch"])
-        roof["ncu_capture"] = {"file": "profiles/r01c_ep1_ncu_summary.json", "duration_us": dur * 1e6,
+        roof["ncu_capture"] = {"file": "profiles/r01d_ep1_ncu_summary.json", "duration_us": dur * 1e6,
                                "dram_bytes": nb, "dram_gbs": nb / dur / 1e9, "dram_frac": nb / dur / 1e9 / hbm_peak,
                                "algorithmic_frac": k_bytes / dur / 1e9 / hbm_peak}
     # layer roofline: slowest of tensor-at-peak, HBM bytes and bytes-over-NVLink (measured peer-store ceiling)
