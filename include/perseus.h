@@ -249,8 +249,9 @@ int perseus_fit_alpha_beta(const double* bytes, const double* ns, size_t n, doub
 
 /* Which forward path the layer runs: fused persistent kernel or stage kernels;
  * CTA-pair (cta_group::2) tiles or 1-CTA tiles (chosen at create: pairs unless
- * PERSEUS_F_NO_PAIR, or each local expert gets at most one 128-row tile and
- * PERSEUS_F_FORCE_PAIR is not set). */
+ * PERSEUS_F_NO_PAIR, or — without PERSEUS_F_FORCE_PAIR — each local expert gets at
+ * most one 128-row tile, or a single-PE layer's Zipf routing leaves the pairs
+ * less than 85% useful (experts with odd tile counts)). */
 int perseus_layer_info(perseus_layer* layer, int* fused, int* cta_pairs);
 
 /* ---- device event log (trace mode) -> the reference's RunTrace ----------

@@ -465,6 +465,23 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
                 sigsim::zipf_route_ids(S, L->E, cfg->skew, L->k,
                                        cfg->seed ^ (0x9E3779B97F4A7C15ULL * uint64_t(rank + 1)), &z);
                 ck(cudaMemcpy(L->zipf_ids, z.data(), z.size() * 4, cudaMemcpyHostToDevice), "memcpy");
+                // EP=1 under skewed routing: experts with an odd tile count make pairs
+                // whose second CTA recomputes the first's rows.  When the pairs'
+                // useful fraction (tiles / 2·pairs) is below 0.85 the 1-CTA kernel is
+                // faster (measured EP=1 Zipf s=1.0 / 1.5: 0.78 / 0.76 useful, 6–14%
+                // faster single; s=0.5: 0.91, pairs 4% faster).  With P > 1 the pair
+                // kernel stayed faster under the same skew (EP=4: 5–7%).
+                if (world == 1 && !(cfg->flags & (PERSEUS_F_NO_PAIR | PERSEUS_F_FORCE_PAIR))) {
+                    std::vector<int64_t> cnt(L->E, 0);
+                    for (int32_t e : z) ++cnt[e];
+                    int64_t tiles = 0, pairs = 0;
+                    for (int64_t n : cnt) {
+                        const int64_t t = (n + kTileRows - 1) / kTileRows;
+                        tiles += t;
+                        pairs += (t + 1) / 2;
+                    }
+                    if (pairs > 0 && double(tiles) < 0.85 * 2.0 * double(pairs)) L->pair = false;
+                }
             }
             L->tm_a1 = make_tmap(L->sym + L->off_heap, 2 * uint64_t(L->R_max), H);
             L->tm_b1 = make_tmap(L->w1, El * 2 * I, H);
