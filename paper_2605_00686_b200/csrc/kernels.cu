@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
 // One CTA per token, one thread per 16-byte column chunk.  Only the (at most
 // k) combine tiles that carry this token's rows are waited on — the tile of
 // sorted slot p is send tile send_first[e] + (p - offsets[e]) / 128.
-template <int K, int CPT>
+template <int K, int CPT, bool CS>
 __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
     // TPC tokens per CTA, TT = H / (8 * CPT) threads per token, CPT 16-byte
     // column chunks per thread (all CPT * k loads in flight)
@@ -439,7 +439,10 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
             w[j] = c.weights[size_t(t) * k + j];
 #pragma unroll
             for (int q = 0; q < CPT; ++q)
-                u[q][j] = *reinterpret_cast<const uint4*>(y + size_t(p) * c.H + (v + q * TT) * 8);
+            {
+                const uint4* src = reinterpret_cast<const uint4*>(y + size_t(p) * c.H + (v + q * TT) * 8);
+                u[q][j] = CS ? __ldcs(src) : *src;  // CS: every y row is read exactly once
+            }
         }
     }
 #pragma unroll
@@ -458,7 +461,9 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
         o.y = pack_bf16(acc[2], acc[3]);
         o.z = pack_bf16(acc[4], acc[5]);
         o.w = pack_bf16(acc[6], acc[7]);
-        *reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + (v + q * TT) * 8) = o;
+        uint4* dst = reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + (v + q * TT) * 8);
+        if (CS) __stcs(dst, o);
+        else *dst = o;
     }
     tl_end(c, kTlCombine, threadIdx.x == 0);
 }
@@ -509,23 +514,33 @@ static int combine_cpt(const DevCtx& c) {
     return (c.H % (8 * cpt) == 0 && c.H / (8 * cpt) <= 1024) ? cpt : 1;
 }
 
-template <int CPT>
+template <int CPT, bool CS>
 static void launch_combine_cpt(const DevCtx& c, cudaStream_t st) {
     const int tt = c.H / (8 * CPT);                 // threads per token
     const int tpc = std::max(1, 256 / tt);          // tokens per CTA
     const dim3 grid((c.S + tpc - 1) / tpc), block(tt * tpc);
     switch (c.k) {
-        case 1: launch_pdl(k_combine<1, CPT>, grid, block, 0, st, c); break;
-        case 2: launch_pdl(k_combine<2, CPT>, grid, block, 0, st, c); break;
-        case 4: launch_pdl(k_combine<4, CPT>, grid, block, 0, st, c); break;
-        case 8: launch_pdl(k_combine<8, CPT>, grid, block, 0, st, c); break;
-        default: launch_pdl(k_combine<0, CPT>, grid, block, 0, st, c); break;
+        case 1: launch_pdl(k_combine<1, CPT, CS>, grid, block, 0, st, c); break;
+        case 2: launch_pdl(k_combine<2, CPT, CS>, grid, block, 0, st, c); break;
+        case 4: launch_pdl(k_combine<4, CPT, CS>, grid, block, 0, st, c); break;
+        case 8: launch_pdl(k_combine<8, CPT, CS>, grid, block, 0, st, c); break;
+        default: launch_pdl(k_combine<0, CPT, CS>, grid, block, 0, st, c); break;
     }
 }
 
+// streaming (evict-first) loads of y and stores of out: y rows and out rows are
+// touched once, so they should not displace the next forward's x / weights in L2.
+// Same-box A/B at EP=1 (tools/ab_combine_cs.sh): combine 40.0 -> 36.8 us.
+// PERSEUS_COMBINE_CS=0 restores plain loads/stores (experiments).
+static bool combine_cs() {
+    static const bool cs = [] { const char* e = getenv("PERSEUS_COMBINE_CS"); return e ? atoi(e) != 0 : true; }();
+    return cs;
+}
+
 void launch_combine(const DevCtx& c, cudaStream_t st) {
-    if (combine_cpt(c) == 2) launch_combine_cpt<2>(c, st);
-    else launch_combine_cpt<1>(c, st);
+    const bool cs = combine_cs();
+    if (combine_cpt(c) == 2) cs ? launch_combine_cpt<2, true>(c, st) : launch_combine_cpt<2, false>(c, st);
+    else cs ? launch_combine_cpt<1, true>(c, st) : launch_combine_cpt<1, false>(c, st);
 }
 
 // Every kernel of the forward asks for the maximum shared-memory carveout, so
@@ -537,6 +552,16 @@ static cudaError_t max_carveout(K* kernel) {
                                 int(cudaSharedmemCarveoutMaxShared));
 }
 
+template <int CPT, bool CS>
+static cudaError_t combine_carveouts() {
+    const cudaError_t es[] = {max_carveout(k_combine<0, CPT, CS>), max_carveout(k_combine<1, CPT, CS>),
+                              max_carveout(k_combine<2, CPT, CS>), max_carveout(k_combine<4, CPT, CS>),
+                              max_carveout(k_combine<8, CPT, CS>)};
+    for (cudaError_t x : es)
+        if (x != cudaSuccess) return x;
+    return cudaSuccess;
+}
+
 cudaError_t configure_kernels(const DevCtx& c) {
     cudaError_t e = cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan_smem_bytes(c)));
     if (e != cudaSuccess) return e;
@@ -544,10 +569,8 @@ cudaError_t configure_kernels(const DevCtx& c) {
                              int(std::max(perm_smem_bytes(c), plan_smem_bytes(c))));
     if (e != cudaSuccess) return e;
     const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_perm), max_carveout(k_plan4), max_carveout(k_dispatch),
-                              max_carveout(k_gate), max_carveout(k_synth_fill), max_carveout(k_combine<0, 1>),
-                              max_carveout(k_combine<1, 1>), max_carveout(k_combine<2, 1>), max_carveout(k_combine<4, 1>),
-                              max_carveout(k_combine<8, 1>), max_carveout(k_combine<0, 2>), max_carveout(k_combine<1, 2>),
-                              max_carveout(k_combine<2, 2>), max_carveout(k_combine<4, 2>), max_carveout(k_combine<8, 2>)};
+                              max_carveout(k_gate), max_carveout(k_synth_fill), combine_carveouts<1, false>(),
+                              combine_carveouts<2, false>(), combine_carveouts<1, true>(), combine_carveouts<2, true>()};
     for (cudaError_t x : es)
         if (x != cudaSuccess) return x;
     return cudaSuccess;
