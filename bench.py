@@ -475,7 +475,7 @@ def main():
             m = json.load(fh)["ncu_full_k_moe2"]
         dur = float(m["metrics"]["gpu__time_duration.sum"][0]) * 1e-6
         nb = float(m["traffic_bytes_per_launch"])
-        roof["ncu_capture"] = {"file": "profiles/r01d_ep1_ncu_summary.json", "duration_us": dur * 1e6,
+        roof["ncu_capture"] = {"file": "profiles/r01e_ep1_ncu_summary.json", "duration_us": dur * 1e6,
                                "dram_bytes": nb, "dram_gbs": nb / dur / 1e9, "dram_frac": nb / dur / 1e9 / hbm_peak,
                                "algorithmic_frac": k_bytes / dur / 1e9 / hbm_peak}
     # layer roofline: slowest of tensor-at-peak, HBM bytes and bytes-over-NVLink (measured peer-store ceiling)
