@@ -105,10 +105,24 @@ uint64_t perseus_fnv1a64(const void* data, size_t len, uint64_t h);
  *   COUPLED   — Put, Fence, Signal per transfer tile (vanilla, protocols.cpp:242-248)
  *   DECOUPLED — Alg. 1: puts + group counter, one fence per group, then the
  *               group's signals (protocols.cpp:250-292); group_size 0 = per PE
- *   NONE      — fault injection: fences suppressed (transport.cpp:104-106) */
+ *   NONE      — fault injection: fences suppressed (transport.cpp:104-106)
+ *   FAULT_EARLY — fault injection: every dispatch flag is written when its
+ *               tile's put is ISSUED (before the data), no fence — the
+ *               "signal before data" bug the ordering checker must catch
+ *               (verify_ordering, metrics.cpp:118-138) */
 #define PERSEUS_SIGNAL_COUPLED 0
 #define PERSEUS_SIGNAL_DECOUPLED 1
 #define PERSEUS_SIGNAL_NONE 2
+#define PERSEUS_SIGNAL_FAULT_EARLY 3
+
+/* group_size of DECOUPLED: 0 = one group per destination PE (assign_groups,
+ * protocols.cpp:65-76); > 0 = fixed-size groups in (dst, expert, tile) order
+ * (:77-88) — must divide every PE's remote tile count in both directions
+ * (ConfigError at create, as run_dispatch's precheck protocols.cpp:348-359);
+ * PERSEUS_GROUP_AUTO = the largest such common divisor g with 8 <= g <=
+ * tiles-per-destination / 4 (>= 8x fewer fences than per tile, >= 4 groups per
+ * destination), else per destination.  Sizes != 0 need balanced / Zipf routing. */
+#define PERSEUS_GROUP_AUTO (-1)
 
 typedef struct perseus_layer_config {
     int64_t hidden_dim;       /* H  (ModelConfig, workload.hpp:16-25) */
@@ -120,7 +134,7 @@ typedef struct perseus_layer_config {
     double skew;              /* Zipf exponent (routing == ZIPF) */
     uint64_t seed;            /* workload seed (config.hpp:36) */
     int32_t signaling;        /* PERSEUS_SIGNAL_* */
-    int64_t group_size;       /* DECOUPLED: 0 = one group per destination PE */
+    int64_t group_size;       /* DECOUPLED: 0 = per destination PE, > 0 fixed, PERSEUS_GROUP_AUTO */
     int32_t flags;            /* PERSEUS_F_* */
 } perseus_layer_config;
 
@@ -128,6 +142,9 @@ typedef struct perseus_layer_config {
 #define PERSEUS_F_UNFUSED 2       /* forward() as stream-ordered stage kernels instead of the fused persistent kernel */
 #define PERSEUS_F_NO_PAIR 4       /* fused kernel on single CTAs (cta_group::1) instead of CTA pairs (cta_group::2) */
 #define PERSEUS_F_FORCE_PAIR 8    /* CTA pairs even when local experts get at most one 128-row tile */
+#define PERSEUS_F_NO_PDL 16       /* no programmatic dependent launch: for several ranks sharing ONE device
+                                     (a grid waiting for its PDL primary holds up the work distributor, so
+                                     another rank's grids the primary waits for may never be scheduled) */
 
 /* Tile granularity: 128 token rows per transfer tile / GEMM M-tile, i.e. the
  * reference's tile_bytes = 128 * H * 2 (workload.hpp:58). */
@@ -254,6 +271,16 @@ int perseus_fit_alpha_beta(const double* bytes, const double* ns, size_t n, doub
  * less than 85% useful (experts with odd tile counts)). */
 int perseus_layer_info(perseus_layer* layer, int* fused, int* cta_pairs);
 
+/* The DECOUPLED signal-group size this layer resolved at create (0 = per
+ * destination PE; PERSEUS_GROUP_AUTO resolved to a size).  1 for the per-tile
+ * protocols. */
+int perseus_layer_group_size(perseus_layer* layer, int64_t* group_size);
+
+/* Host only: the group size perseus_layer_create would resolve for `cfg` at EP
+ * `world` (validation included: ConfigError for a size that does not divide
+ * every PE's remote tile count, or != 0 with learned-gate routing). */
+int perseus_resolve_group_size(const perseus_layer_config* cfg, int world, int64_t* group_size);
+
 /* ---- device event log (trace mode) -> the reference's RunTrace ----------
  * With tracing on, every forward records what the kernels actually did:
  * sender-side puts, fences and flag writes, and receiver-side observations of
@@ -261,8 +288,12 @@ int perseus_layer_info(perseus_layer* layer, int* fused, int* cta_pairs);
  * observation (receive buffers are poisoned before the forward; a signal seen
  * before the data landed is an ordering violation).  Events of one forward,
  * all PEs concatenated, are turned into a sigsim::RunTrace by
- * perseus_trace_analyze, which runs the reference's fence_accounting,
- * verify_ordering and conservation_check on it (metrics.cpp:10-59,118-190). */
+ * perseus_trace_analyze, which runs this library's fence_accounting,
+ * verify_ordering and conservation_check on it (the drop-in restatements of
+ * metrics.cpp:10-59,118-190 in csrc/planner.cpp).  perseus_trace_records hands
+ * out the same records, so the reference's own checkers can be run on them
+ * unmodified (oracle/ref_shim.cpp ref_analyze_records; tests compare the two
+ * field for field). */
 enum {
     PERSEUS_EV_DISPATCH_PUT = 1,    /* sender: a remote transfer tile's stores issued */
     PERSEUS_EV_DISPATCH_FENCE = 2,  /* sender: a group's sys-scope fence */
@@ -310,6 +341,31 @@ typedef struct perseus_trace_report {
  * combine direction mirrors them (same tiles, reversed). */
 int perseus_trace_analyze(const perseus_trace_event* events, size_t n, int nic_ordering,
                           const perseus_transfer* transfers, size_t n_transfers, perseus_trace_report* out);
+/* One sigsim::TraceRecord (trace.hpp:33-46), flattened; enums as the reference's
+ * underlying values (ReqKind: 0 Put, 1 Signal, 2 FenceMarker; TraceKind: 0 Submit,
+ * 1 NicServiceStart, 2 Completion, 3 SignalVisible, ...). */
+typedef struct perseus_trace_record {
+    int64_t time;
+    uint32_t pe;
+    int32_t kind;
+    int32_t req_kind;
+    uint32_t src_pe;
+    uint32_t dst_pe;
+    int32_t fence_flag;
+    uint64_t size;
+    int32_t qp;
+    int32_t pad;
+    int64_t group_id;
+    int64_t tile_id;
+    uint64_t submit_seq;
+} perseus_trace_record;
+
+/* The records of one direction's RunTrace (the one perseus_trace_analyze checks),
+ * plus its total_put_bytes_submitted / _delivered; call with out = NULL to size. */
+int perseus_trace_records(const perseus_trace_event* events, size_t n, int nic_ordering, int direction,
+                          perseus_trace_record* out, size_t cap, size_t* len, uint64_t* submitted_bytes,
+                          uint64_t* delivered_bytes);
+
 /* The same RunTrace of one direction (0 dispatch, 1 combine) in the reference's text
  * format (sigsim::serialize_trace, trace.cpp:33-51); call with buf = NULL to size. */
 int perseus_trace_serialize(const perseus_trace_event* events, size_t n, int nic_ordering, int direction,

@@ -370,6 +370,28 @@ class RefLib:
             C.POINTER(RefLib.RunResult)]
         L.ref_fnv1a64.restype = C.c_uint64
         L.ref_fnv1a64.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64]
+        L.ref_analyze_records.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64, C.POINTER(Transfer),
+                                          C.c_size_t, C.c_int, C.POINTER(RefLib.CheckReport), C.c_char_p,
+                                          C.c_size_t]
+
+    class CheckReport(C.Structure):
+        _fields_ = [(n, C.c_int64) for n in (
+            "fence_count", "flagged_signal_count", "proxy_stop_episodes", "nic_stall_episodes",
+            "proxy_blocked_total_ns", "nic_stall_total_ns", "n_violations", "conservation_pass", "n_failures")]
+
+    def analyze_records(self, records, n, submitted, delivered, transfers, swap=False):
+        """The reference's fence_accounting / verify_ordering / conservation_check
+        (metrics.cpp:10-59,118-190), unmodified, on a RunTrace built from flat
+        records (perseus_trace_record layout); transfers: [m, 6] int64 rows in
+        TransferSpec field order (swap: combine-direction mirror)."""
+        rep = RefLib.CheckReport()
+        arr = Oracle._np_to_transfers(np.asarray(transfers, dtype=np.int64).reshape(-1, 6))
+        msg = C.create_string_buffer(65536)
+        self._chk(self.L.ref_analyze_records(C.addressof(records), n, submitted, delivered, arr,
+                                             len(transfers), int(swap), C.byref(rep), msg, len(msg)))
+        d = {f: getattr(rep, f) for f, _ in RefLib.CheckReport._fields_}
+        d["failures"] = [x for x in msg.value.decode().split("\n") if x]
+        return d
 
 
     def fit_alpha_beta(self, points):

@@ -198,6 +198,89 @@ int ref_fit_alpha_beta(const double* x, const double* y, size_t n, double* out) 
     });
 }
 
+// flat sigsim::TraceRecord, same layout as include/perseus.h:perseus_trace_record
+struct FlatRecord {
+    int64_t time;
+    uint32_t pe;
+    int32_t kind, req_kind;
+    uint32_t src_pe, dst_pe;
+    int32_t fence_flag;
+    uint64_t size;
+    int32_t qp, pad;
+    int64_t group_id, tile_id;
+    uint64_t submit_seq;
+};
+
+struct RefCheckReport {
+    int64_t fence_count, flagged_signal_count, proxy_stop_episodes, nic_stall_episodes;
+    int64_t proxy_blocked_total_ns, nic_stall_total_ns;
+    int64_t n_violations;
+    int64_t conservation_pass;
+    int64_t n_failures;
+};
+
+// The reference's own checkers — sigsim::fence_accounting (metrics.cpp:10-59),
+// verify_ordering (:118-138), conservation_check (:140-190) — run unmodified on
+// a RunTrace built from flat records (e.g. a device RunTrace handed out by
+// perseus_trace_records).  `transfers` = the workload's remote transfers; with
+// `swap` their src/dst are exchanged (the combine direction's mirror).
+// failures: the conservation failure messages, '\n'-joined, into msg[cap].
+int ref_analyze_records(const FlatRecord* recs, size_t n, uint64_t submitted, uint64_t delivered,
+                        const FlatTransfer* t, size_t nt, int swap, RefCheckReport* out, char* msg,
+                        size_t cap) {
+    REF_TRY({
+        sigsim::RunTrace tr;
+        for (size_t i = 0; i < n; ++i) {
+            sigsim::TraceRecord r;
+            r.time = recs[i].time;
+            r.pe = recs[i].pe;
+            r.kind = static_cast<sigsim::TraceKind>(recs[i].kind);
+            r.req_kind = static_cast<sigsim::ReqKind>(recs[i].req_kind);
+            r.src_pe = recs[i].src_pe;
+            r.dst_pe = recs[i].dst_pe;
+            r.size = recs[i].size;
+            r.fence_flag = recs[i].fence_flag != 0;
+            r.qp = recs[i].qp;
+            r.group_id = recs[i].group_id;
+            r.tile_id = recs[i].tile_id;
+            r.submit_seq = recs[i].submit_seq;
+            tr.add(r);
+        }
+        tr.total_put_bytes_submitted = submitted;
+        tr.total_put_bytes_delivered = delivered;
+        sigsim::DispatchWorkload wl;
+        for (size_t i = 0; i < nt; ++i) {
+            sigsim::TransferSpec x;
+            x.src_pe = swap ? t[i].dst_pe : t[i].src_pe;
+            x.dst_pe = swap ? t[i].src_pe : t[i].dst_pe;
+            x.expert = t[i].expert;
+            x.bytes = t[i].bytes;
+            x.tile_id = t[i].tile_id;
+            x.heap_offset = t[i].heap_offset;
+            wl.remote_transfers.push_back(x);
+        }
+        const auto acc = sigsim::fence_accounting(tr);
+        const auto viol = sigsim::verify_ordering(tr);
+        const auto cons = sigsim::conservation_check(tr, wl);
+        out->fence_count = acc.fence_count;
+        out->flagged_signal_count = acc.flagged_signal_count;
+        out->proxy_stop_episodes = acc.proxy_stop_episodes;
+        out->nic_stall_episodes = acc.nic_stall_episodes;
+        out->proxy_blocked_total_ns = acc.proxy_blocked_total;
+        out->nic_stall_total_ns = acc.nic_stall_total;
+        out->n_violations = static_cast<int64_t>(viol.size());
+        out->conservation_pass = cons.pass ? 1 : 0;
+        out->n_failures = static_cast<int64_t>(cons.failures.size());
+        std::string all;
+        for (const auto& f : cons.failures) all += f + "\n";
+        if (msg && cap) {
+            const size_t m = all.size() < cap - 1 ? all.size() : cap - 1;
+            std::memcpy(msg, all.data(), m);
+            msg[m] = 0;
+        }
+    });
+}
+
 // fnv1a64 (trace.cpp:53-62)
 uint64_t ref_fnv1a64(const void* data, size_t len, uint64_t h) {
     return sigsim::fnv1a64(data, len, h);

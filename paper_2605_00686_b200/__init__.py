@@ -5,5 +5,5 @@ Hot path: one MoE-layer forward (gate/route -> dispatch -> SwiGLU expert FFN
 (libperseus.so), behind the reference's sigsim operator API.
 """
 from ._lib import ConfigError, ModelError, VerifyError, lib  # noqa: F401  (fails loudly if the .so is missing)
-from .layer import MoELayer, analyze_trace, serialize_trace  # noqa: F401
+from .layer import MoELayer, analyze_trace, resolve_group_size, serialize_trace, trace_records  # noqa: F401
 from .sigsim import *  # noqa: F401,F403

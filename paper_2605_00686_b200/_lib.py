@@ -13,12 +13,14 @@ LIB_PATH = os.path.join(HERE, "libperseus.so")
 
 OK, ERR_CONFIG, ERR_VERIFY, ERR_RUNTIME = 0, 1, 2, 3
 ROUTE_BALANCED, ROUTE_ZIPF, ROUTE_GATE = 0, 1, 2
-SIGNAL_COUPLED, SIGNAL_DECOUPLED, SIGNAL_NONE = 0, 1, 2
+SIGNAL_COUPLED, SIGNAL_DECOUPLED, SIGNAL_NONE, SIGNAL_FAULT_EARLY = 0, 1, 2, 3
+GROUP_AUTO = -1
 PHASE_ROUTE, PHASE_DISPATCH, PHASE_EXPERT, PHASE_COMBINE, PHASE_ALL = 0, 1, 2, 3, 15
 F_SYNTH_WEIGHTS = 1
 F_UNFUSED = 2
 F_NO_PAIR = 4
 F_FORCE_PAIR = 8
+F_NO_PDL = 16
 TILE_ROWS = 128
 
 
@@ -63,6 +65,14 @@ class TraceReport(C.Structure):
                             "conservation_ok": bool(self.conservation_ok[i]), "put_bytes": self.put_bytes[i]}
         d["conservation_error"] = self.conservation_error.decode()
         return d
+
+
+class TraceRecord(C.Structure):
+    """include/perseus.h:perseus_trace_record (a flat sigsim::TraceRecord)."""
+    _fields_ = [("time", C.c_int64), ("pe", C.c_uint32), ("kind", C.c_int32), ("req_kind", C.c_int32),
+                ("src_pe", C.c_uint32), ("dst_pe", C.c_uint32), ("fence_flag", C.c_int32), ("size", C.c_uint64),
+                ("qp", C.c_int32), ("pad", C.c_int32), ("group_id", C.c_int64), ("tile_id", C.c_int64),
+                ("submit_seq", C.c_uint64)]
 
 
 class LayerConfig(C.Structure):
@@ -125,10 +135,14 @@ def _load():
         "perseus_layer_set_timeline": (C.c_int, [vp, C.c_int]),
         "perseus_layer_set_trace": (C.c_int, [vp, C.c_int]),
         "perseus_layer_info": (C.c_int, [vp, P(C.c_int), P(C.c_int)]),
+        "perseus_layer_group_size": (C.c_int, [vp, P(i64)]),
+        "perseus_resolve_group_size": (C.c_int, [P(LayerConfig), C.c_int, P(i64)]),
         "perseus_layer_read_trace": (C.c_int, [vp, P(TraceEvent), sz, P(sz)]),
         "perseus_fit_alpha_beta": (C.c_int, [P(C.c_double), P(C.c_double), sz, P(C.c_double), P(C.c_double),
                                             P(C.c_double)]),
         "perseus_trace_serialize": (C.c_int, [P(TraceEvent), sz, C.c_int, C.c_int, C.c_char_p, sz, P(sz)]),
+        "perseus_trace_records": (C.c_int, [P(TraceEvent), sz, C.c_int, C.c_int, P(TraceRecord), sz, P(sz), P(u64),
+                                            P(u64)]),
         "perseus_trace_analyze": (C.c_int, [P(TraceEvent), sz, C.c_int, P(Transfer), sz, P(TraceReport)]),
         "perseus_layer_read_timeline": (C.c_int, [vp, P(C.c_uint64), C.c_int]),
     }

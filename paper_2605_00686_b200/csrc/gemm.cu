@@ -114,7 +114,7 @@ __device__ __forceinline__ void finish_tile(const DevCtx& c, const GemmArgs& g, 
         const RecvTile& mt = c.recv[m];
         return c.cflag[mt.src] + size_t(c.par) * c.T_max + mt.tile_id;
     };
-    publish_member_warp(c, grp, c.cgroup_ctr + rt.cgroup, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+    publish_member_warp(c, grp, c.cgroup_ctr + rt.cgroup, flag_of, c.signaling >= PERSEUS_SIGNAL_NONE,
                         kStatCombineFences, kStatCombineSignals);
 }
 
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256, 1)
                 const SendTile& t = c.send[m];
                 return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
             };
-            publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+            publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling >= PERSEUS_SIGNAL_NONE,
                                 kStatDispatchFences, kStatDispatchSignals);
         }
         // the routing weights (router GEMM ran on a side stream), after the puts

@@ -244,8 +244,12 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     }
     __syncthreads();
     if (b == 0 && tid == 0) {
-        // one sys-scope fence, then the per-source ready flag at every PE
-        if (c.P > 1) fence_acq_rel_sys();  // P == 1: the plan kernel is stream-ordered after this one
+        // one fence (cumulative over the CTA barrier above: every thread's
+        // count_table stores), then the per-source ready flag at every PE.  The
+        // plan CTA of this same grid acquires the flag, so even P == 1 needs the
+        // release (gpu scope suffices when no peer reads the table).
+        if (c.P > 1) fence_acq_rel_sys();
+        else fence_acq_rel_gpu();
         for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
         tl_mark(c, kTlCounts);
     }
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
         const SendTile& t = c.send[m];
         return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
     };
-    publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+    publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling >= PERSEUS_SIGNAL_NONE,
                         kStatDispatchFences, kStatDispatchSignals);
 }
 

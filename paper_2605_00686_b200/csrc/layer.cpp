@@ -103,6 +103,7 @@ struct perseus_layer {
     int max_send = 0, max_recv = 0;
     int gate_splits = 1, hist_blocks = 1;
     int num_sms = 148;
+    int64_t gs = 0;  // resolved DECOUPLED group size (resolve_group_size)
     uint32_t epoch = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;                      // router GEMM side stream
@@ -160,7 +161,7 @@ struct perseus_layer {
         c.H = H; c.I = I; c.E = E; c.k = k; c.P = world; c.rank = rank; c.E_loc = El; c.S = S;
         c.routing = cfg.routing;
         c.signaling = cfg.signaling;
-        c.group_size = cfg.signaling == PERSEUS_SIGNAL_DECOUPLED ? int32_t(cfg.group_size) : 1;
+        c.group_size = cfg.signaling == PERSEUS_SIGNAL_DECOUPLED ? int32_t(gs) : 1;
         c.epoch = epoch;
         c.par = int32_t(epoch & 1u);
         c.x = static_cast<const bf16*>(x);
@@ -187,6 +188,7 @@ struct perseus_layer {
         c.self_ready = self_ready; c.sched = sched; c.fwd_t = fwd_t; c.tl = tl;
         c.trace = trace; c.trace_n = trace_n; c.trace_cap = trace_cap; c.trace_seen_ep = trace_seen_ep; c.send_first = send_first; c.pairs = pairs;
         c.stats = stats;
+        c.pdl = (cfg.flags & PERSEUS_F_NO_PDL) ? 0 : 1;
         return c;
     }
 };
@@ -210,8 +212,76 @@ void validate(const perseus_layer_config& c, int rank, int world) {
         throw sigsim::ConfigError("build_dispatch: balanced routing needs E | S*k");
     if (c.routing < 0 || c.routing > 2) throw sigsim::ConfigError("unknown routing mode");
     if (c.routing == PERSEUS_ROUTE_ZIPF && c.skew < 0.0) throw sigsim::ConfigError("zipf_route: exponent must be >= 0");
-    if (c.signaling < 0 || c.signaling > 2) throw sigsim::ConfigError("unknown signaling mode");
-    if (c.group_size < 0) throw sigsim::ConfigError("group size must be >= 0");
+    if (c.signaling < 0 || c.signaling > 3) throw sigsim::ConfigError("unknown signaling mode");
+    if (c.group_size < 0 && c.group_size != PERSEUS_GROUP_AUTO)
+        throw sigsim::ConfigError("group size must be >= 0 (or PERSEUS_GROUP_AUTO)");
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+    while (b) {
+        const int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// Resolve the signal-group size of the DECOUPLED protocol on the host, where the
+// per-(src, expert) counts of the reference routing modes are known for every
+// PE (balanced: exact capacity, workload.cpp:180-195; Zipf: the same seeded
+// draws every rank makes, workload.cpp:186-189).  group_size > 0 must divide
+// every PE's remote tile count in both directions — the reference's own
+// precheck (protocols.cpp:348-359) and assign_groups (:77-88) throw
+// ConfigError otherwise; the device would only flag the plan as bad.
+// PERSEUS_GROUP_AUTO picks the largest common divisor g of those counts with
+// 8 <= g <= (tiles per destination) / 4: at least 8x fewer fences than per tile,
+// and every destination's tiles land in >= 4 groups (an early first group);
+// none exists -> one group per destination.  Learned-gate counts exist only on
+// the device, so fixed / auto sizes need reference routing.
+int64_t resolve_group_size(const perseus_layer_config& c, int world) {
+    if (c.signaling != PERSEUS_SIGNAL_DECOUPLED || c.group_size == 0 || world == 1)
+        return c.group_size == PERSEUS_GROUP_AUTO ? 0 : c.group_size;
+    if (c.routing == PERSEUS_ROUTE_GATE)
+        throw sigsim::ConfigError("group_size != 0 needs reference routing (balanced or zipf): learned-gate "
+                                  "tile counts exist only on the device");
+    const int P = world;
+    const int64_t E = c.experts, S = int64_t(c.tokens_per_pe), k = c.top_k;
+    std::vector<std::vector<int64_t>> cnt(P, std::vector<int64_t>(E, S * k / E));
+    if (c.routing == PERSEUS_ROUTE_ZIPF)
+        for (int s = 0; s < P; ++s) {
+            const auto v = sigsim::zipf_route(uint64_t(S), E, c.skew, k,
+                                              c.seed ^ (0x9E3779B97F4A7C15ULL * uint64_t(s + 1)));
+            for (int64_t e = 0; e < E; ++e) cnt[s][e] = int64_t(v[e]);
+        }
+    // tiles[s][d]: 128-row transfer tiles PE s sends to PE d (workload.cpp:132-151)
+    std::vector<std::vector<int64_t>> tiles(P, std::vector<int64_t>(P, 0));
+    for (int s = 0; s < P; ++s)
+        for (int64_t e = 0; e < E; ++e) tiles[s][e % P] += (cnt[s][e] + kTileRows - 1) / kTileRows;
+    std::vector<int64_t> totals;  // per-PE remote tile counts: dispatch (send) and combine (receive)
+    int64_t min_per_dst = INT64_MAX;
+    for (int s = 0; s < P; ++s) {
+        int64_t snd = 0, rcv = 0;
+        for (int d = 0; d < P; ++d) {
+            if (d == s) continue;
+            snd += tiles[s][d];
+            rcv += tiles[d][s];
+            if (tiles[s][d] > 0) min_per_dst = std::min(min_per_dst, tiles[s][d]);
+        }
+        totals.push_back(snd);
+        totals.push_back(rcv);
+    }
+    if (c.group_size > 0) {
+        for (int64_t n : totals)
+            if (n % c.group_size)
+                throw sigsim::ConfigError("run_dispatch: group size does not divide remote transfer count");
+        return c.group_size;
+    }
+    int64_t g = 0;
+    for (int64_t n : totals) g = gcd64(g, n);
+    const int64_t hi = min_per_dst == INT64_MAX ? 0 : std::max<int64_t>(8, min_per_dst / 4);
+    for (int64_t d = std::min(g, hi); d >= 8; --d)
+        if (g % d == 0) return d;
+    return 0;
 }
 
 template <class T>
@@ -293,7 +363,8 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     const bool tev = all && L->stage_timing;
     if (all) L->timed_last = tev;
     if (tev) ck(cudaEventRecord(L->ev[0], st), "event");
-    if (all && L->tl) ck(cudaMemsetAsync(L->tl, 0, 2 * kTlCount * sizeof(unsigned long long), st), "memset");
+    static const bool tl_keep = [] { const char* e = getenv("PERSEUS_TL_KEEP"); return e && atoi(e) != 0; }();
+    if (all && L->tl && !tl_keep) ck(cudaMemsetAsync(L->tl, 0, 2 * kTlCount * sizeof(unsigned long long), st), "memset");
     if (L->trace && (all || phase == PERSEUS_PHASE_ROUTE)) {
         // trace mode: empty event log, and this forward's receive buffers
         // poisoned (bf16 0xFFFF) so a tile seen before its data shows up
@@ -375,9 +446,11 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
     return guarded([&] {
         *out = nullptr;
         validate(*cfg, rank, world);
+        const int64_t gs = resolve_group_size(*cfg, world);
         auto* L = new perseus_layer;
         try {
             L->cfg = *cfg;
+            L->gs = gs;
             L->fused = !(cfg->flags & PERSEUS_F_UNFUSED);
             // CTA pairs share one expert's weights across two 128-row tiles; when a
             // local expert receives at most one tile per forward on average
@@ -495,6 +568,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             if (world == 1) {
                 L->peer[0] = L->sym;
                 L->connected = true;
+                store_maps(L);
             }
             if (cfg->flags & PERSEUS_F_SYNTH_WEIGHTS) {
                 if (perseus_layer_init_synthetic(L, cfg->seed, nullptr)) throw CudaError(perseus::g_err);
@@ -541,6 +615,7 @@ int perseus_layer_ipc_import(perseus_layer* L, const void* blobs, size_t len_eac
             L->ipc_mapped[p] = true;
         }
         L->connected = true;
+        store_maps(L);  // now, not in the first forward: cudaMalloc may synchronise the device
     });
 }
 
@@ -550,6 +625,11 @@ int perseus_layer_connect_local(perseus_layer* const* ranks, int world) {
             if (ranks[r]->world != world || ranks[r]->rank != r) throw sigsim::ConfigError("rank list mismatch");
             for (int p = 0; p < world; ++p) ranks[r]->peer[p] = ranks[p]->sym;
             ranks[r]->connected = true;
+            ck(cudaSetDevice(ranks[r]->device), "cudaSetDevice");
+            // built here, not in the first forward: ranks sharing one device in this
+            // process are launched back to back, and cudaMalloc may synchronise the
+            // device while an earlier rank's kernels wait for this rank's counts
+            store_maps(ranks[r]);
         }
     });
 }
@@ -759,6 +839,8 @@ int perseus_layer_set_timeline(perseus_layer* L, int on) {
 int perseus_layer_read_timeline(perseus_layer* L, uint64_t* start_end, int n) {
     return guarded([&] {
         if (!L->tl) throw sigsim::ConfigError("timeline is off");
+        ck(cudaSetDevice(L->device), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync");  // the forward ran on non-blocking streams
         std::vector<unsigned long long> h(2 * kTlCount);
         ck(cudaMemcpy(h.data(), L->tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "memcpy");
         for (int i = 0; i < n && i < kTlCount; ++i) {
@@ -775,12 +857,25 @@ int perseus_layer_info(perseus_layer* L, int* fused, int* cta_pairs) {
     });
 }
 
+int perseus_resolve_group_size(const perseus_layer_config* cfg, int world, int64_t* group_size) {
+    return guarded([&] {
+        validate(*cfg, 0, world);
+        *group_size = resolve_group_size(*cfg, world);
+    });
+}
+
+int perseus_layer_group_size(perseus_layer* L, int64_t* group_size) {
+    return guarded([&] { *group_size = L->cfg.signaling == PERSEUS_SIGNAL_DECOUPLED ? L->gs : 1; });
+}
+
 int perseus_layer_set_trace(perseus_layer* L, int on) {
     return guarded([&] {
         ck(cudaSetDevice(L->device), "cudaSetDevice");
         ck(cudaDeviceSynchronize(), "sync");
         if (on && !L->trace) {
-            L->trace_cap = uint32_t(8 * (int64_t(L->max_send) + L->max_recv) + 1024);
+            // per tile: put / signal / fence / observe events, plus the fused kernel's
+            // diagnostic GEMM1-item waits (one per n-block per CTA: I/128 per tile)
+            L->trace_cap = uint32_t((8 + int64_t(L->I) / 128) * (int64_t(L->max_send) + L->max_recv) + 1024);
             ck(cudaMalloc(&L->trace, size_t(L->trace_cap) * sizeof(TraceEv)), "cudaMalloc trace");
             ck(cudaMalloc(&L->trace_n, sizeof(uint32_t)), "cudaMalloc");
             ck(cudaMemset(L->trace_n, 0, sizeof(uint32_t)), "memset");

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <utility>
@@ -79,6 +80,7 @@ struct DevCtx {
     uint32_t trace_cap;
     uint32_t* trace_seen_ep;    // [T_max] combine tiles already observed this forward (epoch-valued)
     unsigned long long* tl;     // [2 * kTlCount] kernel timeline of the last forward (~start, end) or null
+    int32_t pdl;                // launch with programmatic dependent launch (PERSEUS_F_NO_PDL clears it)
 };
 
 // kernel ids of the diagnostic timeline (DevCtx::tl)
@@ -87,10 +89,12 @@ enum TlKernel : int { kTlGate = 0, kTlRoute, kTlPerm, kTlPlan, kTlFused, kTlComb
 
 #ifdef __CUDACC__
 // Launch with programmatic stream serialization (the kernel calls pdl_wait()
-// before touching anything an earlier kernel wrote).
-template <typename... Params, typename... Args>
-inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                              Args&&... args) {
+// before touching anything an earlier kernel wrote) unless the layer runs
+// without PDL (c.pdl == 0: several ranks sharing one device — a grid waiting
+// for its PDL primary's trigger holds up the work distributor, and with it the
+// grids of the other ranks that the primary waits for).
+template <typename K>
+inline cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const DevCtx& c) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -100,8 +104,8 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    cfg.numAttrs = c.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, c);
 }
 
 __device__ __forceinline__ uint64_t fwd_now() {

@@ -158,7 +158,7 @@ __device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, i
         const RecvTile& mt = c.recv[m];
         return c.cflag[mt.src] + size_t(c.par) * c.T_max + mt.tile_id;
     };
-    publish_member_warp(c, grp, c.cgroup_ctr + rt.cgroup, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
+    publish_member_warp(c, grp, c.cgroup_ctr + rt.cgroup, flag_of, c.signaling >= PERSEUS_SIGNAL_NONE,
                         kStatCombineFences, kStatCombineSignals);
     if (lane == 0) atomicMax(c.fwd_t + kFwdCombLast, fwd_now());
 }
@@ -401,6 +401,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         // group must land while the head computes)
         int state = (head_units > 0 && warp < 10) ? 0 : 1;  // 0: self head, 1: remote, 2: self rest
         bool first_remote = true;
+        if (c.signaling == PERSEUS_SIGNAL_FAULT_EARLY) {
+            // fault injection: every remote tile's flag is written as its put is
+            // issued — here, before any row is copied — with no fence: the
+            // "signal before data" bug verify_ordering must catch
+            const int cw = warp < 4 ? warp - 2 : warp - 6;  // 0..5
+            for (int i = (blockIdx.x * 6 + cw) * 32 + lane; i < hdr.n_send_remote; i += gridDim.x * 6 * 32) {
+                const SendTile st = c.send[i];
+                st_relaxed_sys(c.dflag[st.dst] + size_t(c.par) * c.T_max + st.tile_id, c.epoch);
+                atomicAdd(&c.stats[kStatDispatchSignals], 1ull);
+                if (c.trace) trace_ev(c, PERSEUS_EV_DISPATCH_SIGNAL, st.dst, st.tile_id, st.group, 0, 0, fwd_now());
+            }
+        }
         while (true) {
             const bool remote_q = state == 1;
             int u = 0;
@@ -438,6 +450,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 if (lane == 0) atomicMin(c.fwd_t + kFwdDispFirst, fwd_now());
                 first_remote = false;
             }
+            const bool fault_early = c.signaling == PERSEUS_SIGNAL_FAULT_EARLY;  // flags already written
             copy_unit(c, st, r0, nrows, lane);
             __syncwarp();
             uint32_t done = 0;
@@ -455,13 +468,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)st.rows * c.H * 2);
                 if (c.trace) trace_ev(c, PERSEUS_EV_DISPATCH_PUT, st.dst, st.tile_id, st.group, uint32_t(st.rows) * c.H * 2, 0, fwd_now());
             }
-            const Group g = c.groups[st.group];
-            auto flag_of = [&](int m) {
-                const SendTile& t = c.send[m];
-                return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
-            };
-            publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling == PERSEUS_SIGNAL_NONE,
-                                kStatDispatchFences, kStatDispatchSignals);
+            if (!fault_early) {
+                const Group g = c.groups[st.group];
+                auto flag_of = [&](int m) {
+                    const SendTile& t = c.send[m];
+                    return c.dflag[t.dst] + size_t(c.par) * c.T_max + t.tile_id;
+                };
+                publish_member_warp(c, g, c.group_ctr + st.group, flag_of, c.signaling >= PERSEUS_SIGNAL_NONE,
+                                    kStatDispatchFences, kStatDispatchSignals);
+            }
             if (lane == 0) atomicMax(c.fwd_t + kFwdDispLast, fwd_now());
         }
         if (lane == 0) atomicAdd(&c.stats[kStatCopyNs], (unsigned long long)(globaltimer() - tc0));
@@ -679,16 +694,19 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     cfg.dynamicSmemBytes = kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the plan kernel
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
-    attr[1].val.cooperative = 1;
+    int na = 0;
+    if (c.pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the plan kernel
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    attr[na].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
+    attr[na++].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
-        cfg.numAttrs = 1;  // cooperative + clusters rejected: 1 CTA/SM, grid = #SMs keeps them co-resident
+        cfg.numAttrs = na - 1;  // cooperative + clusters rejected: 1 CTA/SM, grid = #SMs keeps them co-resident
         e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
     }
     return e;

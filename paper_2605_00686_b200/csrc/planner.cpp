@@ -385,14 +385,23 @@ ConservationReport conservation_check(const RunTrace& trace, const DispatchWorkl
     if (delivered != trace.total_put_bytes_submitted)
         rep.fail("delivered bytes " + std::to_string(delivered) + " != submitted bytes " +
                  std::to_string(trace.total_put_bytes_submitted));
-    for (const auto& [tile, _] : submitted) {
-        const int c = completed.count(tile) ? completed[tile] : 0;
-        if (c != 1) rep.fail("put tile " + std::to_string(tile) + " completed " + std::to_string(c) + " times");
-        if (!wl.put_only) {
-            const int s = signaled.count(tile) ? signaled[tile] : 0;
-            if (s != 1) rep.fail("tile " + std::to_string(tile) + " signaled " + std::to_string(s) + " times");
-        }
+    // the reference's failure messages, in its order (metrics.cpp:166-188):
+    // every put's completion count first, then every transfer's signal count
+    auto times = [](const std::map<std::int64_t, int>& m, std::int64_t tile) {
+        auto it = m.find(tile);
+        return it == m.end() ? 0 : it->second;
+    };
+    for (const auto& kv : submitted) {
+        const int c = times(completed, kv.first);
+        if (c == 0) rep.fail("put tile " + std::to_string(kv.first) + " has no completion");
+        else if (c != 1) rep.fail("put tile " + std::to_string(kv.first) + " completed " + std::to_string(c) + " times");
     }
+    if (!wl.put_only)
+        for (const auto& kv : submitted) {
+            const int c = times(signaled, kv.first);
+            if (c == 0) rep.fail("transfer tile " + std::to_string(kv.first) + " was never signaled");
+            else if (c != 1) rep.fail("tile " + std::to_string(kv.first) + " signaled " + std::to_string(c) + " times");
+        }
     return rep;
 }
 
@@ -621,6 +630,24 @@ int perseus_trace_analyze(const perseus_trace_event* ev, size_t n, int nic_order
             if (!rep.pass && !out->conservation_error[0] && !rep.failures.empty())
                 std::snprintf(out->conservation_error, sizeof out->conservation_error, "%s: %s",
                               dir == 0 ? "dispatch" : "combine", rep.failures.front().c_str());
+        }
+    });
+}
+
+int perseus_trace_records(const perseus_trace_event* ev, size_t n, int nic_ordering, int direction,
+                          perseus_trace_record* out, size_t cap, size_t* len, uint64_t* submitted_bytes,
+                          uint64_t* delivered_bytes) {
+    return guarded([&] {
+        if (direction != 0 && direction != 1) throw sigsim::ConfigError("direction must be 0 (dispatch) or 1 (combine)");
+        const sigsim::RunTrace tr = device_run_trace(ev, n, direction, nic_ordering, nullptr);
+        *len = tr.records.size();
+        if (submitted_bytes) *submitted_bytes = tr.total_put_bytes_submitted;
+        if (delivered_bytes) *delivered_bytes = tr.total_put_bytes_delivered;
+        if (!out) return;
+        for (size_t i = 0; i < tr.records.size() && i < cap; ++i) {
+            const sigsim::TraceRecord& r = tr.records[i];
+            out[i] = perseus_trace_record{r.time, r.pe, int32_t(r.kind), int32_t(r.req_kind), r.src_pe, r.dst_pe,
+                                          r.fence_flag ? 1 : 0, r.size, r.qp, 0, r.group_id, r.tile_id, r.submit_seq};
         }
     });
 }

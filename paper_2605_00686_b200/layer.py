@@ -37,11 +37,30 @@ def _stream(stream) -> Optional[int]:
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
+def layer_config(model: ModelConfig, tokens_per_pe: int, routing: str = "balanced", skew: float = 0.0,
+                 seed: int = 1, protocol: Optional[ProtocolConfig] = None, flags: int = 0) -> "_lib.LayerConfig":
+    """perseus_layer_config of a layer (include/perseus.h)."""
+    protocol = protocol or combined_protocol(0)
+    return _lib.LayerConfig(model.hidden_dim, model.intermediate_dim, model.experts, model.top_k,
+                            tokens_per_pe, ROUTING[routing], float(skew), seed,
+                            protocol.device_signaling(), protocol.group_size, flags)
+
+
+def resolve_group_size(model: ModelConfig, tokens_per_pe: int, world: int, routing: str = "balanced",
+                       skew: float = 0.0, seed: int = 1, protocol: Optional[ProtocolConfig] = None) -> int:
+    """Host only: the DECOUPLED group size a layer would resolve at create
+    (perseus_resolve_group_size; ConfigError like run_dispatch's precheck)."""
+    cfg = layer_config(model, tokens_per_pe, routing, skew, seed, protocol)
+    g = C.c_int64()
+    check(lib.perseus_resolve_group_size(C.byref(cfg), world, C.byref(g)))
+    return g.value
+
+
 class MoELayer:
     def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
                  device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
                  protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True,
-                 fused: bool = True, pair: Optional[bool] = None):
+                 fused: bool = True, pair: Optional[bool] = None, pdl: bool = True):
         protocol = protocol or combined_protocol(0)
         self.fused = fused
         self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
@@ -51,7 +70,8 @@ class MoELayer:
                                protocol.device_signaling(), protocol.group_size,
                                (_lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
                                | (0 if fused else _lib.F_UNFUSED)
-                               | {None: 0, True: _lib.F_FORCE_PAIR, False: _lib.F_NO_PAIR}[pair])
+                               | {None: 0, True: _lib.F_FORCE_PAIR, False: _lib.F_NO_PAIR}[pair]
+                               | (0 if pdl else _lib.F_NO_PDL))
         self._cfg = cfg
         h = C.c_void_p()
         check(lib.perseus_layer_create(C.byref(cfg), rank, world, device, C.byref(h)))
@@ -175,6 +195,13 @@ class MoELayer:
         check(lib.perseus_layer_info(self._h, C.byref(fused), C.byref(pairs)))
         return {"fused": bool(fused.value), "cta_pairs": bool(pairs.value)}
 
+    def group_size(self) -> int:
+        """The DECOUPLED signal-group size resolved at create (0 = per destination;
+        group_size=-1 / GROUP_AUTO resolved to a size; 1 for per-tile protocols)."""
+        g = C.c_int64()
+        check(lib.perseus_layer_group_size(self._h, C.byref(g)))
+        return g.value
+
     def set_trace(self, on: bool = True) -> None:
         """Device event log of every following forward (puts, fences, flag writes,
         receiver-side first observations with a content check; receive buffers
@@ -259,3 +286,20 @@ def serialize_trace(events: np.ndarray, protocol: ProtocolConfig, direction: int
     buf = C.create_string_buffer(ln.value + 1)
     check(lib.perseus_trace_serialize(ebuf, n, nic, direction, buf, ln.value + 1, C.byref(ln)))
     return buf.value.decode()
+
+
+def trace_records(events: np.ndarray, protocol: ProtocolConfig, direction: int = 0):
+    """One direction's device RunTrace as flat records (perseus_trace_records):
+    (ctypes array of _lib.TraceRecord, n, total_put_bytes_submitted,
+    total_put_bytes_delivered) — what perseus_trace_analyze checks, handed out so
+    the reference's own checkers can run on it."""
+    ev = np.ascontiguousarray(events)
+    n = len(ev)
+    ebuf = (_lib.TraceEvent * max(1, n)).from_buffer_copy(ev.tobytes() or bytes(C.sizeof(_lib.TraceEvent)))
+    ln, sub, dlv = C.c_size_t(0), C.c_uint64(0), C.c_uint64(0)
+    mode = _ordering_mode(protocol)
+    check(lib.perseus_trace_records(ebuf, n, mode, direction, None, 0, C.byref(ln), C.byref(sub), C.byref(dlv)))
+    buf = (_lib.TraceRecord * max(1, ln.value))()
+    check(lib.perseus_trace_records(ebuf, n, mode, direction, buf, ln.value, C.byref(ln), C.byref(sub),
+                                    C.byref(dlv)))
+    return buf, ln.value, sub.value, dlv.value

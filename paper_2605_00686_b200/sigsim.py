@@ -187,8 +187,11 @@ class ProtocolConfig:  # protocols.hpp:20-37
     signaling: str = "coupled"        # coupled | decoupled
     ordering: str = "proxy_fence"     # proxy_fence | nic_fence
     transport: str = "proxy"          # proxy | gpu_direct
-    group_size: int = 0
+    group_size: int = 0               # 0 per destination PE; > 0 fixed; -1 (GROUP_AUTO, layer only) auto
     suppress_fences: bool = False
+    # fault injection beyond the reference's suppress_fences: dispatch flags
+    # written when a tile's put is issued, before its data (PERSEUS_SIGNAL_FAULT_EARLY)
+    fault_early_signal: bool = False
 
     def mode_name(self) -> str:
         if self.transport == "gpu_direct":
@@ -200,6 +203,8 @@ class ProtocolConfig:  # protocols.hpp:20-37
 
     def device_signaling(self) -> int:
         """The device variant this protocol selects (include/perseus.h)."""
+        if self.fault_early_signal:
+            return _lib.SIGNAL_FAULT_EARLY
         if self.suppress_fences:
             return _lib.SIGNAL_NONE
         return _lib.SIGNAL_COUPLED if self.signaling == "coupled" else _lib.SIGNAL_DECOUPLED

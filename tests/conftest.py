@@ -3,6 +3,14 @@ import sys
 
 import pytest
 
+# Several EP ranks share one device in the concurrent GPU tests (gpu_util.
+# run_concurrent), each on its own streams.  With the default 8 hardware
+# connections, streams of different ranks can map onto one connection and be
+# serialised behind each other (a rank's kernels queued behind a peer's kernel
+# that waits for them).  32 connections keep every rank's streams independent.
+# Must be set before the CUDA context exists.
+os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

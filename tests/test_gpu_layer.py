@@ -148,16 +148,27 @@ def test_reference_golden_fences_qwen3_p8_emulated(golden):
             l.close()
 
 
-def test_qwen3_single_gpu_subset(oracle):
-    """The bench workload (Qwen3-30B-A3B shape, S=4096, EP=1): routing
-    bit-exact on all tokens, output vs oracle on a seeded token subset."""
-    from tests.gpu_util import run_emulated, shape_of
+def test_qwen3_bench_config_every_token(oracle):
+    """The bench workload exactly (Qwen3-30B-A3B shape, S=4096, EP=1, balanced
+    routing, the fused CTA-pair kernel the bench times): routing bit-exact and
+    ALL 4096 tokens' outputs vs the fp32 oracle, after repeated forwards."""
+    import torch
+    from tests.gpu_util import shape_of
     pb = _pb()
     m = pb.model_preset("qwen3-30b")
     S = 4096
-    layers, xs, outs = run_emulated(pb, m, S, 1, routing="balanced", seed=1)
-    subset = np.sort(np.random.default_rng(0).choice(S, 48, replace=False))
-    _check_rank(oracle, pb, shape_of(m, S, 1), layers[0], xs[0], outs[0], "balanced", 1, 0.0, 0, subset=subset)
+    l = pb.MoELayer(m, S, routing="balanced", seed=1)
+    assert l.info() == {"fused": True, "cta_pairs": True}
+    x = torch.empty(S, m.hidden_dim, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(x)
+    l.fill_synthetic_x(x, 1)
+    for _ in range(3):
+        l.forward(x, out)
+    torch.cuda.synchronize()
+    c = l.counters()
+    assert c["wait_timeouts"] == 0 and c["errors"] == 0, c
+    _check_rank(oracle, pb, shape_of(m, S, 1), l, x, out, "balanced", 1, 0.0, 0)
+    l.close()
 
 
 @pytest.mark.parametrize("routing,pair", [("balanced", True), ("zipf", True), ("gate", True),

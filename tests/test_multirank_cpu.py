@@ -151,3 +151,40 @@ def test_device_trace_serializes_in_the_reference_format(results):
     assert n_fence == results["vanilla"][1]
     assert len(lines) - 1 == len([e for e in ev if e["kind"] in (1, 2, 3)]) + 2 * len([e for e in ev if e["kind"] == 4])
     assert set(kinds) <= {"submit", "nic_service_start", "signal_visible", "completion"}, set(kinds)
+
+
+@pytest.mark.parametrize("case", CASES + ["missing"])
+def test_reference_checkers_agree_on_the_device_runtrace(case):
+    """The RunTrace the adapter builds (perseus_trace_records) run through the
+    UNMODIFIED reference checkers (oracle/_ref: fence_accounting,
+    verify_ordering, conservation_check, metrics.cpp:10-59,118-190) gives the
+    same fence markers, flagged signals, violations and conservation verdict
+    (first failure message included) as libperseus' perseus_trace_analyze."""
+    from oracle.oracle import RefLib
+    from tests.trace_util import compare_checkers
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefLib()
+    proto = {"vanilla": pb.vanilla_protocol(), "combined": pb.combined_protocol(0),
+             "decoupled_gs2": pb.decoupled_protocol(2), "late": pb.combined_protocol(0),
+             "dup": pb.vanilla_protocol(), "gpu_direct": pb.gpu_direct_protocol(),
+             "missing": pb.vanilla_protocol()}[case]
+    skew = 0.0 if case == "decoupled_gs2" else 1.0
+    wl = pb.build_dispatch(MODEL, pb.ClusterConfig(P, 1, 1), S, skew, 128 * MODEL.hidden_dim * 2, 5)
+    late = wl.remote_transfers[0].tile_id if case == "late" else None
+    dup = wl.remote_transfers[-1].tile_id if case == "dup" else None
+    ev = np.concatenate([_events_for_rank(r, wl, proto, late_tile=late, dup_signal_tile=dup) for r in range(P)])
+    if case == "missing":  # one tile's put never observed at the receiver
+        gone = wl.remote_transfers[1].tile_id
+        ev = ev[~((ev["kind"] == _lib.EV_DISPATCH_SEEN) & (ev["tile"] == gone))]
+    tr = np.array([(t.src_pe, t.dst_pe, t.expert, t.bytes, t.tile_id, t.heap_offset)
+                   for t in wl.remote_transfers], dtype=np.int64).reshape(-1, 6)
+    rep = compare_checkers(pb, ref, ev, proto, tr)
+    if case == "late":
+        assert rep["dispatch"]["ordering_violations"] == 1
+    if case in ("dup", "missing"):
+        assert not rep["dispatch"]["conservation_ok"]
+    if case == "missing":
+        assert "delivered bytes" in rep["conservation_error"], rep["conservation_error"]
+        recs, n, sub, dlv = pb.trace_records(ev, proto, 0)
+        assert f"put tile {gone} has no completion" in ref.analyze_records(recs, n, sub, dlv, tr)["failures"]
