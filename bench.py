@@ -104,6 +104,55 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NvlinkCounters:
+    """Hardware NVLink data counters of one GPU (NVML field values
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, all links, scope UINT_MAX =
+    summed over links): bytes this GPU sent / received over NVLink between two
+    reads.  None when NVML or the fields are unavailable."""
+
+    def __init__(self, device_index: int):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.read()
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        nv = self.nv
+        vals = nv.nvmlDeviceGetFieldValues(self.h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 0xFFFFFFFF),
+                                                    (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 0xFFFFFFFF)])
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                return None
+            out.append(int(v.value.ullVal) * 1024)
+        return out  # [tx_bytes, rx_bytes]
+
+
+def time_blocks(fn, n_blocks, steps, stream, barrier, allmax):
+    """n_blocks x steps back-to-back calls of fn(), each block bracketed by
+    barrier + synchronize and timed with CUDA events on `stream`; returns the
+    per-block ms per step (max over ranks)."""
+    import torch
+    out = []
+    for _ in range(n_blocks):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        barrier()
+        out.append(allmax(a.elapsed_time(b)) / steps)
+    return out
+
+
 # --------------------------------------------------------------- CPU arms ----
 _CPU_CACHE = {}
 
@@ -223,7 +272,8 @@ def main():
                     help="profiling only: override the expert count (e.g. E/4 at EP=1 = one GPU's share at EP=4)")
     ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU (S)")
     ap.add_argument("--signaling", default="combined", choices=["combined", "vanilla", "decoupled"])
-    ap.add_argument("--group-size", type=int, default=0, help="decoupled signal group size (0 = per destination PE)")
+    ap.add_argument("--group-size", type=int, default=0,
+                    help="decoupled signal group size (0 = per destination PE, -1 = auto)")
     ap.add_argument("--routing", default="balanced", choices=["balanced", "zipf", "gate"])
     ap.add_argument("--skew", type=float, default=0.0)
     ap.add_argument("--ref-tokens", type=int, default=1024, help="max tokens per reference-arm step")
@@ -232,6 +282,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="stage kernels instead of the fused persistent kernel")
     ap.add_argument("--no-pair", action="store_true", help="fused kernel on single CTAs instead of CTA pairs")
+    ap.add_argument("--blocks", type=int, default=5, help="repeat blocks timed after the K-step region")
+    ap.add_argument("--block-steps", type=int, default=500, help="forwards per repeat block (>= 200)")
+    ap.add_argument("--no-twin", action="store_true", help="N>1: skip the compute-only twin (exposed comm)")
     ap.add_argument("--variant-steps", type=int, default=200,
                     help="N>1: also time the per-tile-fence (vanilla) variant of the same kernel for this many steps")
     args = ap.parse_args()
@@ -319,10 +372,32 @@ def main():
     ms_step = ms_max / args.steps
     value = world * S * args.steps / (ms_max / 1e3)
 
-    # ---- per-stage times (CUDA events inside the layer, on its stream) ----
+    # ---- repeat blocks (outside the contract's K-step region): >= 3 blocks of
+    # >= 200 back-to-back forwards each, median and min, clocks sampled inside ----
+    n_clk2 = len(clk.lines)
+    nv = NvlinkCounters(local) if world > 1 else None
+    nv0 = nv.read() if nv else None
+    blk_steps = max(200, args.block_steps)
+    blocks = time_blocks(lambda: layer.forward(x, out), args.blocks, blk_steps, stream, barrier, allmax)
+    nv1 = nv.read() if nv else None
+    n_clk3 = len(clk.lines)
+    nvlink_hw = None
+    if nv0 and nv1:
+        # per GPU per forward, from the NVLink hardware counters (all traffic on the links)
+        tx, rx = (nv1[0] - nv0[0]) / (args.blocks * blk_steps), (nv1[1] - nv0[1]) / (args.blocks * blk_steps)
+        nvlink_hw = {"tx_bytes_per_forward": tx, "rx_bytes_per_forward": rx,
+                     "tx_gbs": tx / (statistics.median(blocks) / 1e3) / 1e9,
+                     "source": "NVML NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (all links, KiB counters), rank 0"}
+    timing_blocks = {"blocks": args.blocks, "steps_per_block": blk_steps, "ms_per_step": blocks,
+                     "median_ms": statistics.median(blocks), "min_ms": min(blocks),
+                     "median_tokens_per_s": world * S / (statistics.median(blocks) / 1e3),
+                     "clock_samples_inside": n_clk3 - n_clk2}
+
+    # ---- per-stage times (CUDA events inside the layer, on its stream; they
+    # break the PDL overlap, so a separate pass of >= 200 forwards) ----
     stages = []
     layer.set_stage_timing(True)  # outside the timed region
-    for _ in range(min(args.steps, 10)):
+    for _ in range(max(200, args.block_steps)):
         layer.forward(x, out)
         stages.append(layer.timing())
     stages = np.array(stages)
@@ -400,99 +475,129 @@ def main():
     copy_floor_ms = te_copy / copy_steps * 1e3
     e2e_sync_value = world * S * min(args.steps, 200) / te_sync
 
-    # ---- the per-tile-fence variant of the same kernel (N > 1) ----
-    variant = None
-    if world > 1 and args.variant_steps > 0 and args.signaling != "vanilla":
+    # ---- signalling variants of the same fused kernel (N > 1), same run ----
+    def time_variant(vproto, name):
         vl = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing, skew=args.skew,
-                         seed=1, protocol=pb.vanilla_protocol(), fused=not args.unfused, pair=False if args.no_pair else None)
+                         seed=1, protocol=vproto, fused=not args.unfused, pair=False if args.no_pair else None)
         vl.connect_dist()
         for _ in range(args.warmup):
             vl.forward(x, out)
         barrier()
         v0 = vl.counters()
-        vs, ve = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        vs.record(stream)
-        for _ in range(args.variant_steps):
-            vl.forward(x, out)
-        ve.record(stream)
-        barrier()
+        vb = time_blocks(lambda: vl.forward(x, out), 3, args.variant_steps, stream, barrier, allmax)
         v1 = vl.counters()
-        v_ms = allmax(vs.elapsed_time(ve)) / args.variant_steps
-        vd = {key: (v1[key] - v0[key]) / args.variant_steps for key in ("dispatch_fences", "combine_fences")}
-        variant = {"signaling": "coupled (per-tile fence), same fused kernel", "steps": args.variant_steps,
-                   "ms_per_step": v_ms, "value": world * S / (v_ms / 1e3), "unit": "tokens/s",
-                   "fences_per_forward": vd}
+        n = 3 * args.variant_steps
+        vd = {key: (v1[key] - v0[key]) / n for key in ("dispatch_fences", "combine_fences")}
+        v_ms = statistics.median(vb)
+        res = {"signaling": name, "group_size": vl.group_size(), "steps": n, "ms_per_step": v_ms,
+               "ms_per_step_blocks": vb, "value": world * S / (v_ms / 1e3), "unit": "tokens/s",
+               "fences_per_forward": vd}
         vl.close()
+        return res
+
+    variant = auto_variant = None
+    if world > 1 and args.variant_steps > 0 and args.signaling != "vanilla":
+        variant = time_variant(pb.vanilla_protocol(), "coupled (per-tile fence), same fused kernel")
+        if args.group_size == 0 and args.routing != "gate":
+            auto_variant = time_variant(pb.combined_protocol(-1), "decoupled, auto group size (GROUP_AUTO)")
+
+    # ---- compute-only twin (N > 1): the same per-GPU work, no communication ----
+    # EP = 1 with E / N experts: every local expert receives the same S*k*N/E rows
+    # as at EP = N (balanced routing), so the pair count, GEMM shapes, copy
+    # volume (now all local HBM) and schedule match; dispatch / combine puts,
+    # flags and fences over NVLink disappear.  exposed = T_layer - T_twin, the
+    # twin-run difference the reference's speedup_decomposition uses
+    # (metrics.cpp:97-116).
+    twin = None
+    if world > 1 and not args.no_twin and args.routing == "balanced" and E % world == 0 and \
+            (S * k) % (E // world) == 0:
+        tm = pb.ModelConfig(args.config + "-twin", H, I, E // world, k)
+        tw = pb.MoELayer(tm, S, rank=0, world=1, device=local, routing="balanced", seed=1,
+                         protocol=proto if args.group_size >= 0 else pb.combined_protocol(0),
+                         fused=not args.unfused, pair=False if args.no_pair else None)
+        for _ in range(args.warmup):
+            tw.forward(x, out)
+        tb = time_blocks(lambda: tw.forward(x, out), args.blocks, blk_steps, stream, barrier, allmax)
+        tw.set_stage_timing(True)
+        tst = []
+        for _ in range(200):
+            tw.forward(x, out)
+            tst.append(tw.timing())
+        tw.set_stage_timing(False)
+        tw.close()
+        t_twin = statistics.median(tb)
+        t_layer = timing_blocks["median_ms"]
+        twin = {"what": f"EP=1, E/N={E // world} experts, S={S}: same per-GPU GEMM work, no NVLink",
+                "ms_per_step_blocks": tb, "median_ms": t_twin,
+                "fused_kernel_ms": float(np.mean([t[2] for t in tst])),
+                "exposed_us": (t_layer - t_twin) * 1e3, "exposed_frac": (t_layer - t_twin) / t_layer}
     clk.__exit__(None, None, None)
 
-    # ---- roofline of the dominant kernel ----
-    # fused path: k_moe2 / k_moe (dispatch puts + GEMM1/SwiGLU + GEMM2/combine puts);
-    # unfused path: k_gemm<1> (GEMM1 + SwiGLU).  Algorithmic work per launch on
-    # this GPU (balanced routing: S*k rows received per PE):
-    #   FLOP  = 6*H*I*rows (4HI gate+up, 2HI down)
-    #   bytes = expert weights (E/P)*3*H*I*2 + heap round trip 2*rows*H*2 (dispatch
-    #           write, GEMM1 read) + h round trip 2*rows*I*2 + y write rows*H*2
+    # ---- roofline of the dominant kernel (SURVEY.md §8(d) algorithmic work) ----
+    # fused path: k_moe2 / k_moe (dispatch puts + GEMM1/SwiGLU + GEMM2/combine puts).
+    # Per launch on this GPU (balanced routing: rows = S*k token-expert rows):
+    #   FLOP  = 6*H*I*rows                      (4HI gate+up, 2HI down per row)
+    #   bytes = expert weights (E/P)*3*H*I*2 + x S*H*2 + out S*H*2
+    # The bound is the larger of FLOP / tensor peak and bytes / HBM peak.  The
+    # kernel's own intermediate round trips (heap, h, y) are NOT algorithmic: the
+    # DRAM bytes ncu measured per launch over these bytes is the traffic ratio.
     peaks, peaks_src = measured_peaks()
     rows = S * k
-    tflops_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    tf_burst = peaks.get("bf16_tflops", 1590.0)
+    tf_sust = peaks.get("bf16_tflops_sustained", tf_burst)
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     if not args.unfused:
         kname = "k_moe2 (fused dispatch + GEMM1/SwiGLU + GEMM2/combine-put, tcgen05 cta_group::2)" \
             if layer_info["cta_pairs"] else "k_moe (fused, tcgen05 cta_group::1)"
         k_ms = st_mean[2]
         k_flop = 6.0 * H * I * rows
-        k_bytes = (E // world) * 3.0 * H * I * 2 + 2.0 * rows * H * 2 + 2.0 * rows * I * 2 + rows * H * 2.0
     else:
         kname = "k_gemm<1> (GEMM1 + fused SwiGLU, tcgen05)"
         k_ms = st_mean[2]
         k_flop = 4.0 * H * I * rows
-        k_bytes = (E // world) * 2.0 * H * I * 2 + rows * H * 2.0 + rows * I * 2.0
-    t_tensor = k_flop / (tflops_peak * 1e12)
+    k_bytes = (E // world) * (3.0 if not args.unfused else 2.0) * H * I * 2 + 2.0 * S * H * 2
+    t_tensor = k_flop / (tf_burst * 1e12)
     t_hbm = k_bytes / (hbm_peak * 1e9)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as fh:
-            traffic = json.load(fh).get(f"{args.config}_ep{world}_{'fused' if not args.unfused else 'unfused'}")
     ach_tf = k_flop / (k_ms / 1e3) / 1e12
     ach_gb = k_bytes / (k_ms / 1e3) / 1e9
+    # the committed ncu capture of this kernel at this shape (profiles/): DRAM bytes per launch
+    ncu_file = os.path.join("profiles", f"r02_{args.config}_ep{world}_ncu_summary.json")
+    ncu = None
+    if os.path.exists(os.path.join(ROOT, ncu_file)) and S == 4096 and not args.unfused:
+        with open(os.path.join(ROOT, ncu_file)) as fh:
+            ncu = json.load(fh)
+    traffic = ncu["dram_bytes_per_launch"] if ncu else None
     if t_hbm >= t_tensor:
         roof = {"kernel": kname, "bound": "hbm", "achieved": ach_gb, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach_gb / hbm_peak, "traffic": traffic}
     else:
-        roof = {"kernel": kname, "bound": "tensor", "achieved": ach_tf, "peak": tflops_peak, "unit": "TFLOP/s",
-                "frac": ach_tf / tflops_peak, "traffic": traffic}
-    roof.update({"peak_source": f"{peaks_src} MEASURED_PEAKS.json (hbm_gbs / bf16_tflops_sustained)",
+        roof = {"kernel": kname, "bound": "tensor", "achieved": ach_tf, "peak": tf_burst, "unit": "TFLOP/s",
+                "frac": ach_tf / tf_burst, "traffic": traffic}
+    roof.update({"peak_source": f"{peaks_src} MEASURED_PEAKS.json (bf16_tflops = burst, hbm_gbs)",
+                 "frac_of_sustained_tensor": ach_tf / tf_sust,
                  "launch_ms": k_ms, "algorithmic_flop": k_flop, "algorithmic_bytes": k_bytes,
-                 "tensor": {"achieved_tflops": ach_tf, "frac": ach_tf / tflops_peak},
+                 "algorithmic_basis": "SURVEY.md §8(d): FLOP 6*H*I*S*k; bytes = expert weights + x + out",
+                 "t_tensor_us": t_tensor * 1e6, "t_hbm_us": t_hbm * 1e6,
+                 "tensor": {"achieved_tflops": ach_tf, "frac_burst": ach_tf / tf_burst, "frac_sustained": ach_tf / tf_sust},
                  "hbm": {"achieved_gbs": ach_gb, "frac": ach_gb / hbm_peak},
-                 "timing": "CUDA events on the layer stream around the kernel, mean of 10 synchronised steps"})
-    # the committed ncu capture of the same kernel at this shape (profiles/): its own
-    # duration and DRAM bytes — a short, unthrottled run vs the sustained bench clocks
-    ncu_sum = os.path.join(ROOT, "profiles", "r01d_ep1_ncu_summary.json")
-    if world == 1 and args.config == "qwen3" and not args.unfused and S == 4096 and os.path.exists(ncu_sum):
-        with open(ncu_sum) as fh:
-            m = json.load(fh)["ncu_full_k_moe2"]
-        dur = float(m["metrics"]["gpu__time_duration.sum"][0]) * 1e-6
-        nb = float(m["traffic_bytes_per_launch"])
-        roof["ncu_capture"] = {"file": "profiles/r01e_ep1_ncu_summary.json", "duration_us": dur * 1e6,
-                               "dram_bytes": nb, "dram_gbs": nb / dur / 1e9, "dram_frac": nb / dur / 1e9 / hbm_peak,
-                               "algorithmic_frac": k_bytes / dur / 1e9 / hbm_peak}
-    # layer roofline: slowest of tensor-at-peak, HBM bytes and bytes-over-NVLink (measured peer-store ceiling)
+                 "traffic_ratio": (traffic / k_bytes) if traffic else None,
+                 "timing": f"CUDA events on the layer stream around the kernel, mean of {len(stages)} forwards "
+                           "(separate pass: the events break the PDL chain)"})
+    if ncu:
+        roof["ncu_capture"] = {"file": ncu_file, **{kk: ncu[kk] for kk in ncu if kk != "metrics"}}
+    # layer roofline: slowest of tensor-at-peak, HBM bytes, bytes over NVLink
     flops_layer = 6.0 * H * I * S * k + 2.0 * S * H * E
     nvl_bytes = 2.0 * S * k * (world - 1) / world * H * 2
-    hbm_layer = (E // world) * 3.0 * H * I * 2 + 2.0 * rows * H * 2 + 2.0 * rows * I * 2 + 2.0 * rows * H * 2
-    nvl_bw, nvl_src = 720e9, "assumed"
-    pp = os.path.join(ROOT, "profiles", "r01_nvlink_p2p_bw.json")
-    if os.path.exists(pp):
-        with open(pp) as fh:
-            nvl_bw = max(r["GBps"] for r in json.load(fh)["results"] if r["mode"] == "sm_st16") * 1e9
-        nvl_src = "profiles/r01_nvlink_p2p_bw.json (measured SM peer stores)"
-    t_roof = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / nvl_bw, hbm_layer / (hbm_peak * 1e9))
-    layer_frac = t_roof / (ms_step / 1e3)
+    hbm_layer = (E // world) * 3.0 * H * I * 2 + 2.0 * S * H * 2
+    nvl_bw = 770e9
+    nvl_src = "measured peer copy 770 GB/s per direction (B200_PROFILING.md); own SM-store probe " \
+              "profiles/r01_nvlink_p2p_bw.json: 719 GB/s"
+    t_roof = max(flops_layer / (tf_burst * 1e12), nvl_bytes / nvl_bw, hbm_layer / (hbm_peak * 1e9))
+    t_med = timing_blocks["median_ms"] / 1e3
+    layer_frac = t_roof / t_med
     # north_star's figure: the slower of compute-at-peak and bytes-over-NVLink (no HBM term)
-    t_cn = max(flops_layer / (tflops_peak * 1e12), nvl_bytes / nvl_bw)
-    frac_cn = t_cn / (ms_step / 1e3)
+    t_cn = max(flops_layer / (tf_burst * 1e12), nvl_bytes / nvl_bw)
+    frac_cn = t_cn / t_med
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -524,15 +629,27 @@ def main():
                 "combine_nvlink_gbs": dc["combine_put_bytes"] / dc["combine_span_ns"] if dc["combine_span_ns"] else None,
                 "dispatch_span_us": dc["dispatch_span_ns"] / 1e3, "combine_span_us": dc["combine_span_ns"] / 1e3,
                 "dispatch_bytes": dc["dispatch_put_bytes"], "combine_bytes": dc["combine_put_bytes"],
-                "exposed_dispatch_us": exp_d, "exposed_combine_us": exp_c,
-                "exposed_frac": (exp_d + exp_c) / (ms_step * 1e3),
+                "exposed": ({"us": twin["exposed_us"], "frac": twin["exposed_frac"],
+                             "method": "T_layer - T_compute_only_twin (median of repeat blocks each)"}
+                            if twin else None),
+                "compute_only_twin": twin,
+                "flag_wait_proxy": {"exposed_dispatch_us": exp_d, "exposed_combine_us": exp_c,
+                                    "frac": (exp_d + exp_c) / (ms_step * 1e3),
+                                    "note": "producer waits for remote tiles + longest combine flag wait only; "
+                                            "misses copy-warp issue slots and NVLink/L2 interference"},
+                "nvlink_hw_counters": nvlink_hw,
+                "nvlink_algorithmic_bytes_per_forward": {"dispatch": dc["dispatch_put_bytes"],
+                                                         "combine": dc["combine_put_bytes"],
+                                                         "total": nvl_bytes},
                 "fences_per_forward": {"dispatch": dc["dispatch_fences"], "combine": dc["combine_fences"]},
                 "note": "rank 0's device counters; spans are first remote store -> last remote tile signalled"}
     if variant is not None and dc.get("dispatch_fences"):
         variant["fence_ratio_vs_this_run"] = {
             "dispatch": variant["fences_per_forward"]["dispatch_fences"] / dc["dispatch_fences"],
             "combine": variant["fences_per_forward"]["combine_fences"] / max(dc["combine_fences"], 1e-9)}
-        variant["slowdown_vs_this_run"] = variant["ms_per_step"] / ms_step
+        variant["slowdown_vs_this_run"] = variant["ms_per_step"] / timing_blocks["median_ms"]
+    if auto_variant is not None:
+        auto_variant["speedup_vs_this_run"] = timing_blocks["median_ms"] / auto_variant["ms_per_step"]
     # our kernels per forward: router GEMM, k_route, k_perm (+ the plan CTA), then
     # k_moe2 (fused) or k_dispatch + k_gemm<1> + k_gemm<2> (unfused), then k_combine
     launches_per_step = 5 if not args.unfused else 7
@@ -559,15 +676,18 @@ def main():
             "cta_pairs": layer_info["cta_pairs"],
             "group_size": args.group_size,
             "layer_roofline": {"t_roof_us": t_roof * 1e6, "frac": layer_frac,
+                               "step_basis": "median of the repeat blocks",
                                "frac_of_max_compute_nvlink": frac_cn,
                                "flops": flops_layer, "nvlink_bytes": nvl_bytes, "hbm_bytes": hbm_layer,
-                               "t_tensor_us": flops_layer / (tflops_peak * 1e12) * 1e6,
+                               "t_tensor_us": flops_layer / (tf_burst * 1e12) * 1e6,
                                "t_nvlink_us": nvl_bytes / nvl_bw * 1e6, "nvlink_gbs": nvl_bw / 1e9,
                                "nvlink_source": nvl_src,
                                "t_hbm_us": hbm_layer / (hbm_peak * 1e9) * 1e6},
             "roofline": roof,
             "comm": comm,
             "per_tile_fence_variant": variant,
+            "auto_group_variant": auto_variant,
+            "timing_blocks": timing_blocks,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": S * H * 2,
                     "d2h_bytes_per_step": S * H * 2, "ms_per_step": 1e3 * te_async / args.steps,
                     "api": "perseus_layer_forward_host_async (pinned host buffers, copies pipelined across steps)",
@@ -579,7 +699,8 @@ def main():
                                      "api": "perseus_layer_forward_host (copy in, forward, copy out, sync per call)"}},
             "gpu_launches": launches_per_step * args.steps,
             "per_step_counters": dc,
-            "clocks": dict(clk.summary(), timed_region_samples=n_clk1 - n_clk0),
+            "clocks": dict(clk.summary(), timed_region_samples=n_clk1 - n_clk0,
+                           repeat_block_samples=n_clk3 - n_clk2),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

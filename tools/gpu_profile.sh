@@ -1,10 +1,10 @@
 # bench line + ncu launch list (+ DRAM bytes) + one full ncu capture of the fused kernel (EP=1)
 set -x
-TAG=${TAG:-r01b}
+TAG=${TAG:-r02}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv
 timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; grep '^{' gpurun_out/bench_$TAG.log | tail -c 3000
-B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
+B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --blocks 3 --block-steps 200 --variant-steps 0"
 timeout 300 $B > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -k regex:"k_(gate|route|perm|plan|gemm|combine|moe)" -s 18 -c 18 \

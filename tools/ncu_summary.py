@@ -1,4 +1,4 @@
-"""Build profiles/<TAG>_ep1_ncu_summary.json from the outputs of tools/gpu_profile.sh
+"""Build profiles/<TAG>_qwen3_ep1_ncu_summary.json from the outputs of tools/gpu_profile.sh
 (gpurun_out/launches_<TAG>.csv, prof_moe2_<TAG>.ncu-rep, bench_<TAG>.log), and
 profiles/ncu_traffic.json (roofline.traffic in bench.py).  Runs here (ncu -i reads the
 report without a GPU).
@@ -63,25 +63,36 @@ def main():
     ll = launch_list(os.path.join(OUT, f"launches_{tag}.csv"))
     m, traffic = full_metrics(os.path.join(OUT, f"prof_moe2_{tag}.ncu-rep"))
     bench = [ln for ln in open(os.path.join(OUT, f"bench_{tag}.log")) if ln.startswith("{")]
+    dur_us = float(m["gpu__time_duration.sum"][0]) * SCALE.get(m["gpu__time_duration.sum"][1], 1e-6) / 1e-6 \
+        if m["gpu__time_duration.sum"][1] != "us" else float(m["gpu__time_duration.sum"][0])
+    H, I, E, S, k = 2048, 768, 128, 4096, 8
+    alg = E * 3.0 * H * I * 2 + 2.0 * S * H * 2  # expert weights + x + out
     summary = {
-        "round": 1, "tag": tag, "what": what,
+        "round": 2, "tag": tag, "what": what,
+        "kernel": "k_moe2", "config": "qwen3 EP=1 S=4096 balanced",
+        "duration_us": dur_us, "dram_bytes_per_launch": traffic,
+        "dram_read_bytes": float(m["dram__bytes_read.sum"][0]) * SCALE[m["dram__bytes_read.sum"][1]],
+        "dram_write_bytes": float(m["dram__bytes_write.sum"][0]) * SCALE[m["dram__bytes_write.sum"][1]],
+        "algorithmic_bytes": alg, "traffic_ratio": traffic / alg,
+        "dram_gbs": traffic / (dur_us * 1e-6) / 1e9,
+        "sm_clock_hz": float(m["sm__cycles_elapsed.avg.per_second"][0]) * {"Ghz": 1e9, "Mhz": 1e6, "hz": 1}.get(
+            m["sm__cycles_elapsed.avg.per_second"][1], 1.0),
+        "tensor_pipe_pct": m["sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active"][0],
+        "tensor_mem_cycles_pct": m["sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0],
+        "l2_hit_pct": m["lts__t_sector_hit_rate.pct"][0],
+        "note": "ncu replays are cold-cache and serialised, at the clock ncu saw: compare the DRAM bytes and shares, "
+                "not the absolute duration, with bench.py",
         "ncu_launch_list": {"cmd": "tools/gpu_profile.sh: ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
-                                   "dram__bytes_write.sum --clock-control none -k regex:k_(gate|route|perm|plan|gemm|"
-                                   "combine|moe) -s 18 -c 18 python bench.py --steps 20 --warmup 3 --no-cpu-baseline",
+                                   "dram__bytes_write.sum --clock-control none (fused forward kernels, 3 forwards)",
                             "note": "cold-cache, serialised per-launch times: compare shares, not absolutes",
                             "per_kernel": ll},
         "ncu_full_k_moe2": {"cmd": "ncu --set full --clock-control none --import-source on -k regex:k_moe2 -s 3 -c 1 "
-                                   "python bench.py --steps 20 --warmup 3 --no-cpu-baseline",
-                            "metrics": m, "traffic_bytes_per_launch": traffic},
+                                   "python bench.py (short run, see tools/gpu_profile.sh)",
+                            "metrics": m},
         "bench_line": json.loads(bench[-1]) if bench else None,
     }
-    path = os.path.join(ROOT, "profiles", f"{tag}_ep1_ncu_summary.json")
+    path = os.path.join(ROOT, "profiles", f"{tag}_qwen3_ep1_ncu_summary.json")
     json.dump(summary, open(path, "w"), indent=1)
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    t = json.load(open(tp)) if os.path.exists(tp) else {}
-    t["qwen3_ep1_fused"] = traffic
-    t["_source"] = f"profiles/{tag}_ep1_ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum of one k_moe2 launch (ncu --set full)"
-    json.dump(t, open(tp, "w"), indent=1)
     print(path, {k: v["avg_us"] for k, v in ll.items()}, "traffic", traffic)
 
 
