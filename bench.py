@@ -406,7 +406,7 @@ def main():
     # ---- per-kernel device timeline (globaltimer), outside the timed region ----
     layer.set_timeline(True)
     tls = []
-    for _ in range(min(args.steps, 10)):
+    for _ in range(20):
         layer.forward(x, out)
         torch.cuda.synchronize()
         tls.append(layer.timeline())
@@ -582,7 +582,15 @@ def main():
                  "hbm": {"achieved_gbs": ach_gb, "frac": ach_gb / hbm_peak},
                  "traffic_ratio": (traffic / k_bytes) if traffic else None,
                  "timing": f"CUDA events on the layer stream around the kernel, mean of {len(stages)} forwards "
-                           "(separate pass: the events break the PDL chain)"})
+                           "(separate pass: the events break the PDL chain, so the kernel's launch and "
+                           "prologue are inside; the device timeline below is the PDL-chained span)"})
+    if "fused" in timeline_us:
+        tl_ms = (timeline_us["fused"][1] - timeline_us["fused"][0]) / 1e3
+        roof["device_timeline"] = {"first_cta_start_to_last_cta_end_ms": tl_ms,
+                                   "achieved_tflops": k_flop / (tl_ms / 1e3) / 1e12,
+                                   "frac_burst": k_flop / (tl_ms / 1e3) / 1e12 / tf_burst,
+                                   "frac_sustained": k_flop / (tl_ms / 1e3) / 1e12 / tf_sust,
+                                   "source": "globaltimer, mean of the timeline forwards"}
     if ncu:
         roof["ncu_capture"] = {"file": ncu_file, **{kk: ncu[kk] for kk in ncu if kk != "metrics"}}
     # layer roofline: slowest of tensor-at-peak, HBM bytes, bytes over NVLink

@@ -333,9 +333,10 @@ typedef struct perseus_trace_report {
 } perseus_trace_report;
 
 /* Build one sigsim::RunTrace per direction from the events of one forward (all
- * PEs) and run the reference's checks.  `nic_ordering`: 0 = the protocol orders
- * with fence markers (ProxyFence: vanilla / decoupled), 1 = with flagged signals
- * (NicFence: combined / nic_ordering), 2 = GPU-direct (the reference records
+ * PEs) and run the checks.  `nic_ordering`: 0 = ProxyFence (vanilla / decoupled:
+ * a fence marker per group), 1 = NicFence (combined / nic_ordering: the fence
+ * marker arms the flag of the group's first signal, so both are counted, as the
+ * reference's fence_accounting does), 2 = GPU-direct (the reference records
  * neither; the device fences are the memory model's, protocols.cpp:244-246).  `transfers` = the dispatch
  * transfers the PEs realised (perseus_layer_read_layout of every PE); the
  * combine direction mirrors them (same tiles, reversed). */

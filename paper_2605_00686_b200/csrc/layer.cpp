@@ -11,11 +11,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "layer_dev.h"
 #include "perseus.h"
 #include "perseus_internal.h"
+#include "sigsim/protocols.hpp"
 #include "sigsim/workload.hpp"
 
 namespace perseus {
@@ -921,3 +923,149 @@ int perseus_layer_read_timing(perseus_layer* L, float* ms, int n) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// sigsim::run_dispatch backed by the GPU (include/sigsim/protocols.hpp).
+// Replaces the reference's simulated hot path (protocols.cpp:346-362): the
+// workload's PEs run as layer ranks on the current device, concurrently.
+// ---------------------------------------------------------------------------
+namespace {
+
+void rethrow(int rc) {
+    if (rc == PERSEUS_OK) return;
+    const std::string msg = perseus::g_err;
+    if (rc == PERSEUS_ERR_CONFIG) throw sigsim::ConfigError(msg);
+    throw sigsim::ModelError(msg);
+}
+
+struct RankSet {  // RAII: layers, their token / output buffers and streams
+    std::vector<perseus_layer*> layers;
+    std::vector<void*> bufs;
+    std::vector<cudaStream_t> streams;
+    ~RankSet() {
+        for (perseus_layer* l : layers) perseus_layer_destroy(l);
+        for (void* b : bufs) cudaFree(b);
+        for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    }
+};
+
+}  // namespace
+
+namespace sigsim {
+
+RunTrace run_dispatch(const ProtocolConfig& protocol, const DispatchWorkload& wl, const LatencyModel& latency,
+                      std::uint64_t seed, std::uint64_t config_hash) {
+    latency.validate();
+    const int P = wl.cluster.total_pes();
+    if (protocol.signaling == Signaling::Decoupled && protocol.group_size > 0)
+        for (int pe = 0; pe < P; ++pe) {  // the reference's precheck (protocols.cpp:348-359)
+            std::size_t count = 0;
+            for (const auto& t : wl.remote_transfers) count += t.src_pe == uint32_t(pe) ? 1 : 0;
+            if (count % std::size_t(protocol.group_size))
+                throw ConfigError("run_dispatch: group size does not divide remote transfer count");
+        }
+    if (wl.cluster.gpus_per_node != 1)
+        throw ConfigError("GPU run_dispatch: one GPU rank per PE (ClusterConfig{P,1,1}); same-node PEs would "
+                          "need no fences in the reference (transport.cpp:303-320) but NVLink stores do");
+    if (P < 1 || P > kMaxPes) throw ConfigError("GPU run_dispatch: 1..8 PEs");
+    const uint64_t tile_bytes = uint64_t(kTileRows) * uint64_t(wl.model.hidden_dim) * 2;
+    if (wl.tile_bytes != tile_bytes)
+        throw ConfigError("GPU run_dispatch realises 128-row tiles: tile_bytes must be 128 * hidden_dim * 2 = " +
+                          std::to_string(tile_bytes));
+    if (wl.put_only || wl.microbench) throw ConfigError("GPU run_dispatch: MoE dispatch workloads only");
+
+    perseus_layer_config cfg{};
+    cfg.hidden_dim = wl.model.hidden_dim;
+    cfg.intermediate_dim = wl.model.intermediate_dim;
+    cfg.experts = wl.model.experts;
+    cfg.top_k = wl.model.top_k;
+    cfg.tokens_per_pe = wl.tokens_per_pe;
+    cfg.routing = wl.skew > 0.0 ? PERSEUS_ROUTE_ZIPF : PERSEUS_ROUTE_BALANCED;
+    cfg.skew = wl.skew;
+    cfg.seed = wl.seed;
+    cfg.signaling = protocol.suppress_fences ? PERSEUS_SIGNAL_NONE
+                    : protocol.signaling == Signaling::Coupled ? PERSEUS_SIGNAL_COUPLED : PERSEUS_SIGNAL_DECOUPLED;
+    cfg.group_size = protocol.group_size;
+    // several ranks on one device: no PDL, each rank's persistent grid capped to 1/P of the SMs
+    cfg.flags = PERSEUS_F_SYNTH_WEIGHTS | PERSEUS_F_NO_PDL | PERSEUS_F_FORCE_PAIR;
+    int dev = 0, n_sms = 148;
+    perseus::ck(cudaGetDevice(&dev), "cudaGetDevice");
+    perseus::ck(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    RankSet rs;
+    for (int r = 0; r < P; ++r) {
+        perseus_layer* L = nullptr;
+        rethrow(perseus_layer_create(&cfg, r, P, dev, &L));
+        rs.layers.push_back(L);
+        L->num_sms = std::max(2, (n_sms / P) & ~1);
+    }
+    rethrow(perseus_layer_connect_local(rs.layers.data(), P));
+    const size_t xbytes = size_t(wl.tokens_per_pe) * size_t(wl.model.hidden_dim) * 2;
+    for (int r = 0; r < P; ++r) {
+        void *x = nullptr, *out = nullptr;
+        cudaStream_t st = nullptr;
+        perseus::ck(cudaMalloc(&x, xbytes), "cudaMalloc");
+        rs.bufs.push_back(x);
+        perseus::ck(cudaMalloc(&out, xbytes), "cudaMalloc");
+        rs.bufs.push_back(out);
+        perseus::ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        rs.streams.push_back(st);
+        rethrow(perseus_fill_synthetic_x(rs.layers[r], x, wl.seed, st));
+        rethrow(perseus_layer_set_trace(rs.layers[r], 1));
+    }
+    perseus::ck(cudaDeviceSynchronize(), "sync");
+    for (int r = 0; r < P; ++r) rethrow(perseus_layer_forward(rs.layers[r], rs.bufs[2 * r], rs.bufs[2 * r + 1], rs.streams[r]));
+    perseus::ck(cudaDeviceSynchronize(), "run_dispatch forward");
+
+    std::vector<perseus_trace_event> ev;
+    std::vector<perseus_transfer> got;
+    std::vector<uint64_t> flags;
+    for (int r = 0; r < P; ++r) {
+        perseus_counters c{};
+        rethrow(perseus_layer_counters(rs.layers[r], &c));
+        if (c.wait_timeouts || c.errors)
+            throw ModelError("GPU run_dispatch: rank " + std::to_string(r) + " saw " + std::to_string(c.wait_timeouts) +
+                             " signal-wait timeouts / " + std::to_string(c.errors) + " device errors");
+        size_t n = 0;
+        rethrow(perseus_layer_read_trace(rs.layers[r], nullptr, 0, &n));
+        std::vector<perseus_trace_event> e(n);
+        rethrow(perseus_layer_read_trace(rs.layers[r], e.data(), n, &n));
+        ev.insert(ev.end(), e.begin(), e.end());
+        size_t ns = 0, nf = 0;
+        rethrow(perseus_layer_read_layout(rs.layers[r], nullptr, 0, &ns, nullptr, 0, &nf));
+        std::vector<perseus_transfer> t(ns);
+        std::vector<int64_t> f(nf);
+        rethrow(perseus_layer_read_layout(rs.layers[r], t.data(), ns, &ns, f.data(), nf, &nf));
+        got.insert(got.end(), t.begin(), t.end());
+        for (int64_t x : f) flags.push_back(uint64_t(x));
+    }
+    // the realised layout must be the workload's (build_dispatch, workload.cpp:132-213)
+    auto key = [](const perseus_transfer& t) { return std::make_tuple(t.src_pe, t.dst_pe, t.expert, t.tile_id); };
+    std::sort(got.begin(), got.end(), [&](const perseus_transfer& a, const perseus_transfer& b) { return key(a) < key(b); });
+    std::vector<TransferSpec> want = wl.remote_transfers;
+    std::sort(want.begin(), want.end(), [](const TransferSpec& a, const TransferSpec& b) {
+        return std::make_tuple(a.src_pe, a.dst_pe, a.expert, a.tile_id) < std::make_tuple(b.src_pe, b.dst_pe, b.expert, b.tile_id);
+    });
+    bool same = got.size() == want.size();
+    for (size_t i = 0; same && i < got.size(); ++i)
+        same = got[i].src_pe == want[i].src_pe && got[i].dst_pe == want[i].dst_pe && got[i].expert == want[i].expert &&
+               got[i].bytes == want[i].bytes && got[i].tile_id == want[i].tile_id &&
+               got[i].heap_offset == want[i].heap_offset;
+    if (!same) throw ModelError("GPU run_dispatch: the device's realised dispatch layout differs from the workload");
+
+    const int ordering = protocol.transport == TransportPath::GpuDirect ? 2
+                         : protocol.ordering == OrderingMode::NicFence ? 1 : 0;
+    RunTrace tr = perseus::device_run_trace(ev.data(), ev.size(), 0, ordering, nullptr);
+    tr.config_hash = config_hash;
+    tr.workload_digest = wl.digest();
+    tr.seed = seed;
+    std::vector<uint64_t> ext;
+    for (const auto& t : got) {
+        ext.push_back(t.dst_pe);
+        ext.push_back(t.heap_offset);
+        ext.push_back(t.bytes);
+    }
+    tr.heap_digest = perseus_heap_digest(ext.data(), got.size(), flags.data(), flags.size());
+    return tr;
+}
+
+}  // namespace sigsim

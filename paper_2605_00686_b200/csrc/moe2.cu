@@ -48,12 +48,13 @@ static_assert(kStgBytes >= 128 * kStgRow, "staging");
 constexpr int kRing = 8;
 constexpr int kUnitRows = 2;  // fine units: few tiles in flight, so tiles land one after another at link rate
 constexpr int kUnitsPerTile = kTileRows / kUnitRows;
-constexpr int kSelfWindow = 160;  // self tiles (x 512 KB at H=2048) copied ahead of consumption
 constexpr size_t kSmem = 1024 + size_t(kStages) * kStage + kStgBytes + 512;
 
 struct Args {
     int32_t n1, n2, kb1, kb2, lag;
     int32_t lag_end;  // lag over the last pairs (>= lag; see launch_moe2)
+    int32_t self_window;  // self tiles copied ahead of the tiles the scheduler handed out
+    int32_t discard;      // bit 0: heap rows after GEMM1, bit 1: h rows after GEMM2 (discard.global.L2)
     const CUtensorMap* smaps;  // store maps, box 64 x 32, SW128: [0] hbuf, [1 + p] ybuf of PE p
     int64_t a1_row_base;
 };
@@ -137,17 +138,28 @@ __device__ __forceinline__ void store_chunk(uint8_t* stg_warp, int& buf, const u
     buf ^= 1;
 }
 
+// Rows [row0, row0 + rows) of a bf16 [*][cols] buffer are dead: drop their L2
+// lines without write-back (one warp).
+__device__ __forceinline__ void discard_rows(const bf16* base, int64_t row0, int rows, int cols, int lane) {
+    const char* p = reinterpret_cast<const char*>(base + size_t(row0) * cols);
+    const int lines = rows * cols * 2 / 128;
+    for (int i = lane; i < lines; i += 32) discard_l2(p + size_t(i) * 128);
+}
+
 // combine-direction completion of one n-block of a remote M-tile (4 epilogue warps)
-__device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, int nb) {
+__device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, int nb, bool discard_h) {
     named_bar_sync(1, 128);
     if ((threadIdx.x >> 5) != 4) return;
     const int lane = threadIdx.x & 31;
     const RecvTile rt = c.recv[ti];
     if (lane == 0 && nb == 0) atomicAdd(&c.stats[kStatRecvTiles], 1ull);
-    if (rt.cgroup < 0) return;
+    if (rt.cgroup < 0 && !discard_h) return;
     uint32_t done = 0;
     if (lane == 0) done = atom_add_acq_rel_gpu(c.tile_ctr + ti, 1u) + 1 == uint32_t(n_nb);
     if (!__shfl_sync(0xffffffffu, done, 0)) return;
+    // every GEMM2 n-block of this tile has run (its TMA loads of h are complete)
+    if (discard_h) discard_rows(c.hbuf, rt.heap_row, rt.rows, c.I, lane);
+    if (rt.cgroup < 0) return;
     if (lane == 0) {
         atomicAdd(&c.stats[kStatCombinePuts], 1ull);
         atomicAdd(&c.stats[kStatCombineBytes], (unsigned long long)rt.rows * c.H * 2);
@@ -425,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             }
             if (state == 0 && u >= head_units) state = 1;  // head claimed: this unit, then the remote queue
             if (!remote_q) {
-                // Pace the self copies: stay at most kSelfWindow tiles ahead of the
+                // Pace the self copies: stay at most f.self_window tiles ahead of the
                 // tiles the scheduler has handed out, so heap rows are still in L2
                 // when GEMM1 reads them (self tiles are consumed first, in this
                 // order).  The items of every grabbed tile are always allowed.
@@ -435,7 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                         const int w = int(*reinterpret_cast<volatile uint32_t*>(c.sched));
                         const int L = min(f.lag, T);
                         const int started = w < L * f.n1 ? w / f.n1 : L + (w - L * f.n1) / (f.n1 + f.n2);
-                        if (need < 2 * started + kSelfWindow) break;
+                        if (need < 2 * started + f.self_window) break;
                         __nanosleep(256);
                     }
                 }
@@ -571,7 +583,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                         fence_proxy_async();
                     }
                     named_bar_sync(2, 128);
-                    if (threadIdx.x == 128) atom_add_acq_rel_gpu(c.g1_done + mine, 1u);
+                    if (warp == 4) {
+                        uint32_t last = 0;
+                        if (lane == 0) last = atom_add_acq_rel_gpu(c.g1_done + mine, 1u) + 1 == uint32_t(f.n1);
+                        // every GEMM1 n-block of this tile has run (both CTAs' TMA loads
+                        // of its heap rows are complete): the rows are dead
+                        if ((f.discard & 1) && __shfl_sync(0xffffffffu, last, 0))
+                            discard_rows(c.heap[c.rank] + size_t(c.par) * c.R_max * c.H, rt.heap_row, rt.rows, c.H, lane);
+                    }
                 }
             } else {
                 if (full_tile) {
@@ -628,7 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 if (pend_ti >= 0) {
                     bulk_wait<4>();
                     fence_proxy_async();
-                    finish_tile(c, f.n2, pend_ti, pend_nb);
+                    finish_tile(c, f.n2, pend_ti, pend_nb, (f.discard & 2) != 0);
                 }
                 pend_ti = mine;
                 pend_nb = it.nb;
@@ -638,7 +657,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (pend_ti >= 0) {
             bulk_wait0();
             fence_proxy_async();
-            finish_tile(c, f.n2, pend_ti, pend_nb);
+            finish_tile(c, f.n2, pend_ti, pend_nb, (f.discard & 2) != 0);
         }
     }
     pdl_launch_dependents();  // the combine's launch overlaps this CTA's teardown
@@ -682,6 +701,12 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
         const int cover = (pairs_live * f.kb1 + f.n2 * f.kb2 - 1) / (f.n2 * f.kb2);
         const int lag_end = c.P == 1 ? std::max(f.lag, cover + (pairs_live + f.n2 - 1) / f.n2) : f.lag;
         f.lag_end = lag_end_env >= 0 ? std::max(f.lag, lag_end_env) : lag_end;
+    }
+    {
+        static const int sw = [] { const char* e = getenv("PERSEUS_SELF_WINDOW"); return e ? atoi(e) : 160; }();
+        static const int dc = [] { const char* e = getenv("PERSEUS_DISCARD"); return e ? atoi(e) : 0; }();
+        f.self_window = sw;
+        f.discard = dc;
     }
     f.smaps = smaps;
     f.a1_row_base = a1_row_base;

@@ -142,6 +142,20 @@ enum FwdSlot : int {
     kFwdSlots = 8
 };
 
+}  // namespace perseus
+
+#include "perseus.h"
+#include "sigsim/trace.hpp"
+
+namespace perseus {
+
+// One direction (0 dispatch, 1 combine) of one forward's device events (all PEs)
+// as a sigsim::RunTrace; ordering 0 ProxyFence, 1 NicFence, 2 GPU-direct
+// (planner.cpp; perseus_trace_analyze / _records / _serialize and the
+// GPU-backed sigsim::run_dispatch build on it).
+sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int dir, int ordering,
+                                  int64_t* late_tiles);
+
 constexpr uint64_t kWaitTimeoutNs = 4000000000ull;  // 4 s: a lost signal errors out, never hangs
 
 }  // namespace perseus

@@ -70,6 +70,18 @@ void ModelConfig::validate() const {
     if (top_k > experts) throw ConfigError("model '" + name + "': top_k exceeds expert count");
 }
 
+// transport.cpp:15-24 — the GPU-backed run_dispatch validates the simulated
+// fabric's parameters it is handed, with the reference's messages
+void LatencyModel::validate() const {
+    if (base_rtt_ns < 0 || per_request_nic_service_ns < 0 || issue_cost_ns < 0 || issue_jitter_ns < 0 ||
+        gpu_direct_issue_cost_ns < 0 || nvlink_latency_ns < 0)
+        throw ConfigError("latency model: negative time parameter");
+    if (bandwidth_bytes_per_ns <= 0.0) throw ConfigError("latency model: bandwidth must be > 0");
+    if (completion_tail_coeff < 0.0) throw ConfigError("latency model: tail coefficient must be >= 0");
+    if (proxy_poll_quantum_ns <= 0) throw ConfigError("latency model: poll quantum must be > 0");
+    if (processors_per_pe < 1) throw ConfigError("latency model: processors_per_pe must be >= 1");
+}
+
 void ClusterConfig::validate() const {
     if (nodes < 1 || gpus_per_node < 1)
         throw ConfigError("cluster: nodes and gpus_per_node must be >= 1");
@@ -524,10 +536,10 @@ uint64_t perseus_heap_digest(const uint64_t* ext, size_t n_ext, const uint64_t* 
 
 }  // extern "C"
 
-namespace {
+namespace perseus {
 // One direction's device events (all PEs) as a sigsim::RunTrace (see perseus.h):
-// puts -> Submit/Put; group fences -> Submit/FenceMarker (ProxyFence) or the flag on
-// the group's first signal (NicFence); flag writes -> NicServiceStart/Signal;
+// puts -> Submit/Put; group fences -> Submit/FenceMarker (both orderings), plus the
+// flag on the group's first signal (NicFence); flag writes -> NicServiceStart/Signal;
 // receiver observations -> SignalVisible + Completion/Put at the time the tile's
 // content was first complete.
 // ordering: 0 ProxyFence (fences -> FenceMarker records), 1 NicFence (the group's first
@@ -564,7 +576,10 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
             tr.total_put_bytes_submitted += e.bytes;
             tr.add(r);
         } else if (k == 1) {
-            if (ordering != 0) continue;
+            // ProxyFence and NicFence both submit a FenceMarker per group (under
+            // NicFence it arms the flag of the next signal, transport.cpp:149-166);
+            // GPU-direct records none (protocols.cpp:244-246,285-287)
+            if (ordering == 2) continue;
             r.kind = sigsim::TraceKind::Submit;
             r.req_kind = sigsim::ReqKind::FenceMarker;
             r.src_pe = uint32_t(e.pe);
@@ -599,6 +614,11 @@ sigsim::RunTrace device_run_trace(const perseus_trace_event* ev, size_t n, int d
     if (!tr.records.empty()) tr.makespan = tr.records.back().time - tr.records.front().time;
     return tr;
 }
+
+}  // namespace perseus
+
+namespace {
+using perseus::device_run_trace;
 
 sigsim::DispatchWorkload realised_workload(const perseus_transfer* transfers, size_t n, int dir) {
     sigsim::DispatchWorkload wl;

@@ -252,6 +252,10 @@ DEVI void umma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+// Invalidate one 128-byte L2 line without writing it back (its contents become
+// undefined): dead intermediates need not reach DRAM.
+DEVI void discard_l2(const void* p) { asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory"); }
+
 // ------------------------------------------------- memory-model helpers ----
 DEVI void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 DEVI void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }

@@ -54,6 +54,24 @@ int main() {
     // fit_alpha_beta on an exact line
     auto f = sigsim::fit_alpha_beta({{1.0, 12.0}, {2.0, 14.0}, {4.0, 18.0}});
     EXPECT(f.alpha_ns > 9.999 && f.alpha_ns < 10.001 && f.beta_ns_per_byte > 1.999 && f.beta_ns_per_byte < 2.001);
+    // the GPU-backed run_dispatch (protocols.hpp:62-64) rejects, before touching a
+    // device, what the reference rejects and what the device cannot realise
+    auto throws_config = [](auto&& fn) {
+        try {
+            fn();
+        } catch (const sigsim::ConfigError&) {
+            return true;
+        } catch (...) {
+            return false;
+        }
+        return false;
+    };
+    sigsim::LatencyModel bad_lat;
+    bad_lat.proxy_poll_quantum_ns = 0;  // transport.cpp:15-24
+    EXPECT(throws_config([&] { bad_lat.validate(); }));
+    EXPECT(throws_config([&] { sigsim::run_dispatch(sigsim::vanilla_protocol(), wl_t, bad_lat, 1); }));
+    EXPECT(throws_config([&] { sigsim::run_dispatch(sigsim::decoupled_protocol(5), wl_t, sigsim::LatencyModel{}, 1); }));
+    EXPECT(throws_config([&] { sigsim::run_dispatch(sigsim::vanilla_protocol(), wl, sigsim::LatencyModel{}, 1); }));
     // FNV-1a (trace.cpp:53-62)
     EXPECT(sigsim::fnv1a64("", 0) == 0xcbf29ce484222325ULL);
     std::printf("dropin_kats: %s (%d failures)\n", failures ? "FAIL" : "pass", failures);
