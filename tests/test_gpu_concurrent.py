@@ -81,11 +81,13 @@ def _check_all(oracle, pb, m, S, P, layers, xs, outs, routing, seed, skew, proto
     (4, "balanced", 0.0, "combined", 0),
     (4, "gate", 0.0, "decoupled", 0),
     (4, "balanced", 0.0, "combined", -1),
+    (8, "balanced", 0.0, "combined", 0),
+    (8, "zipf", 1.5, "vanilla", 0),
 ])
 def test_concurrent_fused_ranks_qwen3(oracle, P, routing, skew, proto, gsz):
     """Qwen3-30B-A3B layer shape (BASELINE configs[1]), S = 1024 tokens per rank,
-    P ranks concurrently on the fused CTA-pair kernel, 2 forwards (both
-    symmetric buffer halves)."""
+    P ranks concurrently on the fused CTA-pair kernel (P = 8: the headline EP,
+    18 SMs per rank), 2 forwards (both symmetric buffer halves)."""
     from tests.gpu_util import run_concurrent
     pb = _pb()
     m = pb.ModelConfig("qwen3", **{"hidden_dim": QWEN3["H"], "intermediate_dim": QWEN3["I"],
@@ -132,7 +134,8 @@ def _trace_run(pb, oracle, P, protocol, trials, S=1024):
     return reps, counters
 
 
-@pytest.mark.parametrize("P,proto", [(2, "combined"), (2, "vanilla"), (4, "combined"), (4, "decoupled")])
+@pytest.mark.parametrize("P,proto", [(2, "combined"), (2, "vanilla"), (4, "combined"), (4, "decoupled"),
+                                     (8, "combined")])
 def test_concurrent_device_trace_safe_protocols(oracle, P, proto):
     """The fused kernel's device event log of concurrent forwards -> RunTrace ->
     fence_accounting / verify_ordering / conservation_check (libperseus' and the
