@@ -142,6 +142,14 @@ typedef struct perseus_layer_config {
 #define PERSEUS_F_UNFUSED 2       /* forward() as stream-ordered stage kernels instead of the fused persistent kernel */
 #define PERSEUS_F_NO_PAIR 4       /* fused kernel on single CTAs (cta_group::1) instead of CTA pairs (cta_group::2) */
 #define PERSEUS_F_FORCE_PAIR 8    /* CTA pairs even when local experts get at most one 128-row tile */
+/* compute-only twins (diagnostics; outputs are NOT the layer's): one
+ * direction's peer stores and flag writes go to this rank's own buffers and its
+ * receivers do not wait for that direction's flags — the same per-GPU kernels,
+ * schedule and copy volume without the NVLink traffic.  T_layer - T_twin is the
+ * exposed communication (the reference's twin-run decomposition,
+ * metrics.cpp:97-116). */
+#define PERSEUS_F_LOCAL_DISPATCH 32
+#define PERSEUS_F_LOCAL_COMBINE 64
 #define PERSEUS_F_NO_PDL 16       /* no programmatic dependent launch: for several ranks sharing ONE device
                                      (a grid waiting for its PDL primary holds up the work distributor, so
                                      another rank's grids the primary waits for may never be scheduled) */

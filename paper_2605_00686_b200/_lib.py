@@ -21,6 +21,8 @@ F_UNFUSED = 2
 F_NO_PAIR = 4
 F_FORCE_PAIR = 8
 F_NO_PDL = 16
+F_LOCAL_DISPATCH = 32
+F_LOCAL_COMBINE = 64
 TILE_ROWS = 128
 
 

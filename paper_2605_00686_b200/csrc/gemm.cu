@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(256, 1)
                 const CUtensorMap* ta;
                 const CUtensorMap* tb;
                 if (it.kind == 1) {
-                    const bool ok = rt.tile_id >= 0 ? wait_flag_geq(dflags + rt.tile_id, c.epoch, kWaitTimeoutNs)
+                    const bool ok = rt.tile_id >= 0 ? (c.local_dispatch || wait_flag_geq(dflags + rt.tile_id, c.epoch, kWaitTimeoutNs))
                                                     : wait_flag_geq(c.self_ready + p, c.epoch, kWaitTimeoutNs);
                     if (!ok) atomicAdd(&c.stats[kStatTimeouts], 1ull);
                     a_row = int32_t(f.a1_row_base + rt.heap_row);

@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
     const bool live = t < c.S;
     uint64_t t_start = 0;
     if (c.P > 1 && threadIdx.x == 0) t_start = fwd_now();
-    if (c.P > 1 && live && v < k) {
+    if (c.P > 1 && live && v < k && !c.local_combine) {
         const int e = c.ids[size_t(t) * k + v];
         if (e % c.P != c.rank) {
             const int32_t rel = c.pos[size_t(t) * k + v] - c.offsets[e];

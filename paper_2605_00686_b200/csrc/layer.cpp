@@ -177,11 +177,17 @@ struct perseus_layer {
             uint8_t* b = peer[p];
             c.count_table[p] = reinterpret_cast<int32_t*>(b + off_ctab);
             c.count_flag[p] = reinterpret_cast<uint32_t*>(b + off_cflag_cnt);
-            c.heap[p] = reinterpret_cast<bf16*>(b + off_heap);
-            c.dflag[p] = reinterpret_cast<uint32_t*>(b + off_dflag);
-            c.ybuf[p] = reinterpret_cast<bf16*>(b + off_ybuf);
-            c.cflag[p] = reinterpret_cast<uint32_t*>(b + off_cflag);
+            // compute-only twins (diagnostics): a direction's peer stores and flags
+            // go to this rank's own buffers instead (the receivers skip those waits)
+            uint8_t* bd = (cfg.flags & PERSEUS_F_LOCAL_DISPATCH) ? peer[rank] : b;
+            uint8_t* bc = (cfg.flags & PERSEUS_F_LOCAL_COMBINE) ? peer[rank] : b;
+            c.heap[p] = reinterpret_cast<bf16*>(bd + off_heap);
+            c.dflag[p] = reinterpret_cast<uint32_t*>(bd + off_dflag);
+            c.ybuf[p] = reinterpret_cast<bf16*>(bc + off_ybuf);
+            c.cflag[p] = reinterpret_cast<uint32_t*>(bc + off_cflag);
         }
+        c.local_dispatch = (cfg.flags & PERSEUS_F_LOCAL_DISPATCH) ? 1 : 0;
+        c.local_combine = (cfg.flags & PERSEUS_F_LOCAL_COMBINE) ? 1 : 0;
         c.R_max = R_max; c.T_max = T_max; c.Y_rows = Y_rows;
         c.hdr = hdr; c.send = send; c.groups = groups; c.recv = recv; c.cgroups = cgroups;
         c.group_ctr = group_ctr; c.cgroup_ctr = cgroup_ctr; c.tile_ctr = tile_ctr;
@@ -330,8 +336,10 @@ const CUtensorMap* store_maps(perseus_layer* L) {
     if (!L->smaps) {
         std::vector<CUtensorMap> m(1 + kMaxPes);
         m[0] = make_tmap(L->hbuf, uint64_t(L->R_max), uint64_t(L->I), 32);
+        const bool local_c = (L->cfg.flags & PERSEUS_F_LOCAL_COMBINE) != 0;
         for (int p = 0; p < L->world; ++p)
-            m[1 + p] = make_tmap(L->peer[p] + L->off_ybuf, 2 * uint64_t(L->Y_rows), uint64_t(L->H), 32);
+            m[1 + p] = make_tmap((local_c ? L->peer[L->rank] : L->peer[p]) + L->off_ybuf, 2 * uint64_t(L->Y_rows),
+                                 uint64_t(L->H), 32);
         void* d = nullptr;
         ck(cudaMalloc(&d, m.size() * sizeof(CUtensorMap)), "cudaMalloc store maps");
         ck(cudaMemcpy(d, m.data(), m.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice), "memcpy store maps");

@@ -80,6 +80,8 @@ struct DevCtx {
     uint32_t trace_cap;
     uint32_t* trace_seen_ep;    // [T_max] combine tiles already observed this forward (epoch-valued)
     unsigned long long* tl;     // [2 * kTlCount] kernel timeline of the last forward (~start, end) or null
+    int32_t local_dispatch;     // compute-only twin: dispatch puts / flags stay local, remote tiles not awaited
+    int32_t local_combine;      // compute-only twin: combine puts / flags stay local, combine flags not awaited
     int32_t pdl;                // launch with programmatic dependent launch (PERSEUS_F_NO_PDL clears it)
 };
 

@@ -55,6 +55,7 @@ struct Args {
     int32_t lag_end;  // lag over the last pairs (>= lag; see launch_moe2)
     int32_t self_window;  // self tiles copied ahead of the tiles the scheduler handed out
     int32_t discard;      // bit 0: heap rows after GEMM1, bit 1: h rows after GEMM2 (discard.global.L2)
+    int32_t remote_warps; // copy warps (of 6) that take remote dispatch units
     const CUtensorMap* smaps;  // store maps, box 64 x 32, SW128: [0] hbuf, [1 + p] ybuf of PE p
     int64_t a1_row_base;
 };
@@ -303,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 const uint64_t tw0 = globaltimer();
                 if (cur.kind == 1) {
                     const int tile_id = c.recv[cur.mine].tile_id;
-                    const bool ok = tile_id >= 0 ? wait_flag_geq(dflags + tile_id, c.epoch, kWaitTimeoutNs)
+                    const bool ok = tile_id >= 0 ? (c.local_dispatch || wait_flag_geq(dflags + tile_id, c.epoch, kWaitTimeoutNs))
                                                  : wait_flag_geq(c.self_ready + cur.mine, c.epoch, kWaitTimeoutNs);
                     if (!ok) atomicAdd(&c.stats[kStatTimeouts], 1ull);
                     const uint64_t dw = globaltimer() - tw0;
@@ -411,7 +412,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const uint64_t tc0 = globaltimer();
         // warps 10-11 open the remote stream at once (the first destination's
         // group must land while the head computes)
-        int state = (head_units > 0 && warp < 10) ? 0 : 1;  // 0: self head, 1: remote, 2: self rest
+        // f.remote_warps of the 6 copy warps (warps 11, 10, 9, ... first) take remote units
+        const bool remote_ok = (warp < 4 ? warp - 2 : warp - 6) >= 6 - f.remote_warps;
+        int state = (head_units > 0 && warp < 10) ? 0 : (remote_ok ? 1 : 2);  // 0: self head, 1: remote, 2: self rest
         bool first_remote = true;
         if (c.signaling == PERSEUS_SIGNAL_FAULT_EARLY) {
             // fault injection: every remote tile's flag is written as its put is
@@ -432,10 +435,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             u = __shfl_sync(0xffffffffu, u, 0);
             if (u >= (remote_q ? remote_units : self_units)) {
                 if (state == 2) break;
-                state = state == 0 ? 1 : 2;
+                state = (state == 0 && remote_ok) ? 1 : 2;
                 continue;
             }
-            if (state == 0 && u >= head_units) state = 1;  // head claimed: this unit, then the remote queue
+            if (state == 0 && u >= head_units) state = remote_ok ? 1 : 2;  // head claimed: this unit, then the remote queue
             if (!remote_q) {
                 // Pace the self copies: stay at most f.self_window tiles ahead of the
                 // tiles the scheduler has handed out, so heap rows are still in L2
@@ -705,8 +708,10 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
     {
         static const int sw = [] { const char* e = getenv("PERSEUS_SELF_WINDOW"); return e ? atoi(e) : 160; }();
         static const int dc = [] { const char* e = getenv("PERSEUS_DISCARD"); return e ? atoi(e) : 0; }();
+        static const int rw = [] { const char* e = getenv("PERSEUS_REMOTE_WARPS"); return e ? atoi(e) : 6; }();
         f.self_window = sw;
         f.discard = dc;
+        f.remote_warps = std::max(1, std::min(6, rw));
     }
     f.smaps = smaps;
     f.a1_row_base = a1_row_base;

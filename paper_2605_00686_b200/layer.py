@@ -60,7 +60,7 @@ class MoELayer:
     def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
                  device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
                  protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True,
-                 fused: bool = True, pair: Optional[bool] = None, pdl: bool = True):
+                 fused: bool = True, pair: Optional[bool] = None, pdl: bool = True, flags: int = 0):
         protocol = protocol or combined_protocol(0)
         self.fused = fused
         self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
@@ -71,7 +71,7 @@ class MoELayer:
                                (_lib.F_SYNTH_WEIGHTS if synthetic_weights else 0)
                                | (0 if fused else _lib.F_UNFUSED)
                                | {None: 0, True: _lib.F_FORCE_PAIR, False: _lib.F_NO_PAIR}[pair]
-                               | (0 if pdl else _lib.F_NO_PDL))
+                               | (0 if pdl else _lib.F_NO_PDL) | flags)
         self._cfg = cfg
         h = C.c_void_p()
         check(lib.perseus_layer_create(C.byref(cfg), rank, world, device, C.byref(h)))
