@@ -396,7 +396,8 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     {
         const double t_tile = 128.0 * L->H * 2 / 600e9;                   // NVLink store rate per sender
         const double t_pair = 2.0 * 128 * 6.0 * L->H * L->I / 1.0e15;      // GPU-wide: pairs complete at ~1 PFLOP/s
-        c.head_ratio = float(t_tile / t_pair);
+        static const double scale = [] { const char* e = getenv("PERSEUS_HEAD_SCALE"); return e ? atof(e) : 1.0; }();
+        c.head_ratio = float(scale * t_tile / t_pair);
     }
     if (all || phase == PERSEUS_PHASE_ROUTE) {
         if (L->cfg.routing == PERSEUS_ROUTE_GATE) {
