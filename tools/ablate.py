@@ -29,8 +29,8 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", default="256,1024,4096,16384")
-    ap.add_argument("--modes", default="vanilla,perseus,gsdiv",
-                    help="vanilla | perseus (per destination) | gsN | gsdiv (every power-of-two divisor)")
+    ap.add_argument("--modes", default="vanilla,perseus,auto,gsdiv",
+                    help="vanilla | perseus (per destination) | auto (GROUP_AUTO) | gsN | gsdiv (every power-of-two divisor)")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "ablation.csv"))
     args = ap.parse_args()
@@ -62,6 +62,8 @@ def main():
                 proto = pb.vanilla_protocol()
             elif mode == "perseus":
                 proto = pb.combined_protocol(0)
+            elif mode == "auto":  # PERSEUS_GROUP_AUTO, resolved on the host like the layer does
+                proto = pb.combined_protocol(pb.resolve_group_size(model, S, world, protocol=pb.combined_protocol(-1)))
             else:
                 proto = pb.combined_protocol(int(mode[2:]))
             n_own = sum(1 for t in wl.remote_transfers if t.src_pe == rank)
@@ -90,7 +92,8 @@ def main():
             d = {k: (c1[k] - c0[k]) / args.steps for k in c1}
             assert d["wait_timeouts"] == 0 and d["errors"] == 0, d
             own_bytes = sum(t.bytes for t in wl.remote_transfers if t.src_pe == rank)
-            row = dict(P=world, S=S, mode=proto.mode_name() + (f"_gs{proto.group_size}" if proto.group_size else ""),
+            row = dict(P=world, S=S, mode=proto.mode_name() + (f"_gs{proto.group_size}" if proto.group_size else "")
+                       + ("_auto" if mode == "auto" else ""),
                        bytes=own_bytes,
                        dispatch_fences=d["dispatch_fences"], combine_fences=d["combine_fences"],
                        ref_fences=ref_f, signals=d["dispatch_signals"], us=float(ms.item()) * 1e3,
