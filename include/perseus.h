@@ -148,6 +148,11 @@ typedef struct perseus_layer_config {
  * schedule and copy volume without the NVLink traffic.  T_layer - T_twin is the
  * exposed communication (the reference's twin-run decomposition,
  * metrics.cpp:97-116). */
+/* one PE, CTA-pair kernel: the fused kernel combines each token as soon as its
+ * k expert rows exist (a ready queue fed by GEMM2 tile completions, copy warps as
+ * combiners) instead of the combine kernel after it; same bits.  Experimental:
+ * slower at the bench shape. */
+#define PERSEUS_F_DF_COMBINE 128
 #define PERSEUS_F_LOCAL_DISPATCH 32
 #define PERSEUS_F_LOCAL_COMBINE 64
 #define PERSEUS_F_NO_PDL 16       /* no programmatic dependent launch: for several ranks sharing ONE device

@@ -23,6 +23,7 @@ F_FORCE_PAIR = 8
 F_NO_PDL = 16
 F_LOCAL_DISPATCH = 32
 F_LOCAL_COMBINE = 64
+F_DF_COMBINE = 128
 TILE_ROWS = 128
 
 

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
         const int64_t flat = int64_t(t) * c.k + lane;
         my_id = c.routing == PERSEUS_ROUTE_BALANCED ? int(flat % c.E) : c.zipf_ids[flat];
     }
+    if (lane == 0 && c.tok_ready) c.tok_ready[t] = 0;  // dataflow combine: this forward's row count
     if (lane < c.k) {
         c.ids[size_t(t) * c.k + lane] = my_id;
         // per-256-token-block expert histogram (this forward's parity half)

@@ -141,6 +141,9 @@ struct perseus_layer {
     bool pair = true;   // ... on CTA pairs (cta_group::2)
     int32_t* pairs = nullptr;
     unsigned long long* stats = nullptr;
+    int32_t* tok_ready = nullptr;             // dataflow combine (one PE): per-token rows written
+    unsigned long long* ready_q = nullptr;    // ... tokens in readiness order
+    bool df_combine = false;
 
     // symmetric region
     uint8_t* sym = nullptr;
@@ -197,6 +200,9 @@ struct perseus_layer {
         c.trace = trace; c.trace_n = trace_n; c.trace_cap = trace_cap; c.trace_seen_ep = trace_seen_ep; c.send_first = send_first; c.pairs = pairs;
         c.stats = stats;
         c.pdl = (cfg.flags & PERSEUS_F_NO_PDL) ? 0 : 1;
+        c.df_combine = df_combine ? 1 : 0;
+        c.tok_ready = df_combine ? tok_ready : nullptr;
+        c.ready_q = ready_q;
         return c;
     }
 };
@@ -310,7 +316,7 @@ void free_layer(perseus_layer* L) {
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
                     L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl, L->smaps, L->trace, L->trace_n, L->trace_seen_ep,
-                    L->send_first, L->pairs};
+                    L->send_first, L->pairs, L->tok_ready, L->ready_q};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : L->ev)
@@ -427,7 +433,7 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
                "launch k_moe");
         if (tev) ck(cudaEventRecord(L->ev[3], st), "event");
         if (tev) ck(cudaEventRecord(L->ev[4], st), "event");
-        launch_combine(c, st);
+        if (!c.df_combine) launch_combine(c, st);  // else the fused kernel combined every token
         if (tev) ck(cudaEventRecord(L->ev[5], st), "event");
         ck(cudaGetLastError(), "kernel launch");
         return;
@@ -527,11 +533,13 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->send_done = dalloc<uint32_t>(L->max_send);
             L->g1_done = dalloc<uint32_t>(L->max_recv);
             L->self_ready = dalloc<uint32_t>(L->max_recv);
-            L->sched = dalloc<uint32_t>(4);
+            L->sched = dalloc<uint32_t>(8);
             L->fwd_t = dalloc<unsigned long long>(kFwdSlots);
             L->send_first = dalloc<int32_t>(E);
             L->pairs = dalloc<int32_t>(2 * size_t(L->max_recv) + 4);
             L->stats = dalloc<unsigned long long>(kStatCount);
+            L->tok_ready = dalloc<int32_t>(S);
+            L->ready_q = dalloc<unsigned long long>(S);
 
             // symmetric region: identical layout on every rank
             size_t o = 0;
@@ -567,6 +575,12 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
                     if (pairs > 0 && double(tiles) < 0.85 * 2.0 * double(pairs)) L->pair = false;
                 }
             }
+            // PERSEUS_F_DF_COMBINE (one PE, CTA pairs): the fused kernel combines
+            // tokens as their rows complete instead of a combine kernel after it.
+            // Off by default: measured slower (Qwen3 EP=1: the fused kernel grows
+            // by ~75 us vs a 30 us combine kernel; the last pairs' GEMM2 — a third
+            // of the tokens' last rows — comes at the end of the schedule anyway)
+            L->df_combine = (cfg->flags & PERSEUS_F_DF_COMBINE) && world == 1 && L->fused && L->pair;
             L->tm_a1 = make_tmap(L->sym + L->off_heap, 2 * uint64_t(L->R_max), H);
             L->tm_b1 = make_tmap(L->w1, El * 2 * I, H);
             L->tm_a2 = make_tmap(L->hbuf, uint64_t(L->R_max), I);

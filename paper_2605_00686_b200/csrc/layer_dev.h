@@ -80,6 +80,11 @@ struct DevCtx {
     uint32_t trace_cap;
     uint32_t* trace_seen_ep;    // [T_max] combine tiles already observed this forward (epoch-valued)
     unsigned long long* tl;     // [2 * kTlCount] kernel timeline of the last forward (~start, end) or null
+    // dataflow combine (one PE, CTA-pair kernel): the fused kernel combines every
+    // token as soon as its k expert rows exist, instead of a combine kernel after it
+    int32_t df_combine;
+    int32_t* tok_ready;             // [S] expert rows of the token written this forward
+    unsigned long long* ready_q;    // [S] (epoch << 32 | token), in readiness order
     int32_t local_dispatch;     // compute-only twin: dispatch puts / flags stay local, remote tiles not awaited
     int32_t local_combine;      // compute-only twin: combine puts / flags stay local, combine flags not awaited
     int32_t pdl;                // launch with programmatic dependent launch (PERSEUS_F_NO_PDL clears it)
@@ -176,24 +181,30 @@ __device__ __forceinline__ void trace_seen(const DevCtx& c, int kind, int src, i
              t_seen);
 }
 
-// Routing weights of token t: softmax over its k chosen experts' logits (the
-// sum of the router's split-K partials in fixed order) -> weights[t][0..k).
-// One warp; lane j < k handles choice j.  (orc_route_weights)
-__device__ __forceinline__ void route_weights_warp(const DevCtx& c, int t, int lane) {
-    float mine = -INFINITY;
+// Routing weights of token t by one warp: lane j < k holds the logit of its
+// j-th expert (the router's split-K partials summed in fixed order); every lane
+// then forms the max and the sum of exponentials SEQUENTIALLY in j (values
+// broadcast one by one), as orc_route_weights does, so all lanes — and every
+// kernel using this (k_route, the fused kernel's dataflow combine) — get the
+// same bits.  Returns lane j's weight (0 for lanes >= k).
+__device__ __forceinline__ float route_weight_lane(const DevCtx& c, int t, int lane) {
+    float l = -INFINITY;
     if (lane < c.k) {
         const int e = c.ids[size_t(t) * c.k + lane];
-        mine = 0.f;
-        for (int q = 0; q < c.gate_splits; ++q) mine += c.logits[(size_t(q) * c.S + t) * c.E + e];
+        l = 0.f;
+        for (int q = 0; q < c.gate_splits; ++q) l += c.logits[(size_t(q) * c.S + t) * c.E + e];
     }
-    float m = mine;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float ex = lane < c.k ? expf(mine - m) : 0.f;
-    float s = ex;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane < c.k) c.weights[size_t(t) * c.k + lane] = ex / s;
+    float m = -INFINITY;
+    for (int j = 0; j < c.k; ++j) m = fmaxf(m, __shfl_sync(0xffffffffu, l, j));
+    float s = 0.f;
+    for (int j = 0; j < c.k; ++j) s += expf(__shfl_sync(0xffffffffu, l, j) - m);
+    return lane < c.k ? expf(l - m) / s : 0.f;
+}
+
+// ... and stores it: weights[t][j] = lane j's weight
+__device__ __forceinline__ void route_weights_warp(const DevCtx& c, int t, int lane) {
+    const float w = route_weight_lane(c, t, lane);
+    if (lane < c.k) c.weights[size_t(t) * c.k + lane] = w;
 }
 #endif
 

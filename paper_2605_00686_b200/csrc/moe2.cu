@@ -148,6 +148,46 @@ __device__ __forceinline__ void discard_rows(const bf16* base, int64_t row0, int
     for (int i = lane; i < lines; i += 32) discard_l2(p + size_t(i) * 128);
 }
 
+// One token's combine by one warp (dataflow combine): routing weights (when the
+// router ran on a side stream; lane j holds w[j]), then out[t] = sum_j w[j] *
+// y[pos(t, j)] in j order with fmaf in fp32 -> bf16 — k_combine's arithmetic —
+// one 16-byte chunk per lane per step with the token's k rows in flight.  KM >= k.
+template <int KM>
+__device__ __forceinline__ void combine_token_warp(const DevCtx& c, int t, int lane) {
+    const int k = c.k;
+    float wl;
+    if (c.weights_late) {
+        wl = route_weight_lane(c, t, lane);
+        if (lane < k) c.weights[size_t(t) * k + lane] = wl;
+    } else {
+        wl = lane < k ? c.weights[size_t(t) * k + lane] : 0.f;
+    }
+    const int32_t pl = lane < k ? c.pos[size_t(t) * k + lane] : 0;
+    const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
+    const int nvec = c.H / 8;
+    for (int v0 = lane; v0 < nvec; v0 += 32) {
+        uint4 a[KM];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const int32_t pj = __shfl_sync(0xffffffffu, pl, j);
+            if (j < k) a[j] = __ldcs(reinterpret_cast<const uint4*>(y + size_t(pj) * c.H) + v0);
+        }
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const float wj = __shfl_sync(0xffffffffu, wl, j);
+            if (j < k) {
+                const bf16* x = reinterpret_cast<const bf16*>(&a[j]);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = __fmaf_rn(wj, __bfloat162float(x[q]), acc[q]);
+            }
+        }
+        __stcs(reinterpret_cast<uint4*>(c.out + size_t(t) * c.H) + v0,
+               make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
+                          pack_bf16(acc[6], acc[7])));
+    }
+}
+
 // combine-direction completion of one n-block of a remote M-tile (4 epilogue warps)
 __device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, int nb, bool discard_h) {
     named_bar_sync(1, 128);
@@ -155,12 +195,25 @@ __device__ __forceinline__ void finish_tile(const DevCtx& c, int n_nb, int ti, i
     const int lane = threadIdx.x & 31;
     const RecvTile rt = c.recv[ti];
     if (lane == 0 && nb == 0) atomicAdd(&c.stats[kStatRecvTiles], 1ull);
-    if (rt.cgroup < 0 && !discard_h) return;
+    if (rt.cgroup < 0 && !discard_h && !c.df_combine) return;
     uint32_t done = 0;
     if (lane == 0) done = atom_add_acq_rel_gpu(c.tile_ctr + ti, 1u) + 1 == uint32_t(n_nb);
     if (!__shfl_sync(0xffffffffu, done, 0)) return;
-    // every GEMM2 n-block of this tile has run (its TMA loads of h are complete)
+    // every GEMM2 n-block of this tile has run (its TMA loads of h are complete;
+    // its y rows are written: each n-block's stores completed + proxy fence before
+    // its release on tile_ctr, which the acquire above observed)
     if (discard_h) discard_rows(c.hbuf, rt.heap_row, rt.rows, c.I, lane);
+    if (c.df_combine) {
+        // dataflow combine: one more expert row of each of the tile's tokens; a token
+        // whose k rows all exist goes on the ready queue (release -> the combiner's acquire)
+        for (int r = lane; r < rt.rows; r += 32) {
+            const int32_t t = c.rows[rt.ybuf_row + r];
+            if (int(atom_add_acq_rel_gpu(reinterpret_cast<uint32_t*>(c.tok_ready) + t, 1u)) + 1 == c.k) {
+                const uint32_t slot = atomicAdd(&c.sched[4], 1u);
+                st_release_gpu_u64(c.ready_q + slot, (static_cast<unsigned long long>(c.epoch) << 32) | uint32_t(t));
+            }
+        }
+    }
     if (rt.cgroup < 0) return;
     if (lane == 0) {
         atomicAdd(&c.stats[kStatCombinePuts], 1ull);
@@ -535,8 +588,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             atomicMax(c.tl + 2 * kTlCopyEnd, ~fwd_now());
             atomicMax(c.tl + 2 * kTlCopyEnd + 1, fwd_now());
         }
-        // the routing weights (router GEMM ran on a side stream), after the puts
-        if (c.weights_late) {
+        if (c.df_combine) {
+            // dataflow combine: take tokens in the order their k expert rows were
+            // completed; out[t] = sum_j w[t][j] * y[pos(t, j)] in fixed j order (fmaf),
+            // exactly k_combine's arithmetic
+            while (true) {
+                uint32_t i = 0;
+                if (lane == 0) i = atomicAdd(&c.sched[5], 1u);
+                i = __shfl_sync(0xffffffffu, i, 0);
+                if (i >= uint32_t(c.S)) break;
+                unsigned long long v = 0;
+                if (lane == 0) {
+                    const uint64_t t0 = globaltimer();
+                    while (uint32_t((v = ld_acquire_gpu_u64(c.ready_q + i)) >> 32) != c.epoch) {
+                        if (globaltimer() - t0 > kWaitTimeoutNs) {
+                            atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                            break;
+                        }
+                        __nanosleep(128);
+                    }
+                }
+                v = __shfl_sync(0xffffffffu, v, 0);
+                if (uint32_t(v >> 32) != c.epoch) continue;
+                if (c.k <= 8) combine_token_warp<8>(c, int(uint32_t(v)), lane);
+                else combine_token_warp<16>(c, int(uint32_t(v)), lane);
+            }
+        } else if (c.weights_late) {
+            // the routing weights (router GEMM ran on a side stream), after the puts
             const int cw = warp < 4 ? warp - 2 : warp - 6;  // 0..5
             for (int t = blockIdx.x * 6 + cw; t < c.S; t += gridDim.x * 6) route_weights_warp(c, t, lane);
         }

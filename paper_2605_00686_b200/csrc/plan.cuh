@@ -93,7 +93,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     for (int i = tid; i < PE; i += kPlanThreads) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
     if (tid == 0) {
         #pragma unroll 1
-        for (int q = 0; q < 4; ++q) c.sched[q] = 0;
+        for (int q = 0; q < 8; ++q) c.sched[q] = 0;  // work items, copy queues, dataflow-combine queue
         #pragma unroll 1
         for (int q = 0; q < kFwdSlots; ++q) c.fwd_t[q] = (q & 1) || q == kFwdDoneCtas ? 0ull : ~0ull;  // min / max
     }

@@ -332,3 +332,31 @@ def test_c_abi_only_program(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "layer_c_abi: pass" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("routing", ["balanced", "zipf"])
+def test_dataflow_combine_bit_identical(oracle, routing):
+    """PERSEUS_F_DF_COMBINE (one PE): tokens combined inside the fused kernel as
+    their rows complete give exactly the combine kernel's outputs and weights."""
+    import torch
+    from paper_2605_00686_b200 import _lib
+    from tests.gpu_util import bf16_bits
+    pb = _pb()
+    m = pb.model_preset("qwen3-30b")
+    S = 2048
+    res = []
+    for fl in (0, _lib.F_DF_COMBINE):
+        l = pb.MoELayer(m, S, routing=routing, skew=1.1, seed=8, pair=True, flags=fl)
+        x = torch.empty(S, m.hidden_dim, dtype=torch.bfloat16, device="cuda")
+        o = torch.empty_like(x)
+        l.fill_synthetic_x(x, 8)
+        for _ in range(3):
+            l.forward(x, o)
+        torch.cuda.synchronize()
+        c = l.counters()
+        assert c["wait_timeouts"] == 0 and c["errors"] == 0, c
+        res.append((bf16_bits(o), l.routing()[1]))
+        l.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
