@@ -104,6 +104,39 @@ __global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const 
 }
 
 // ----------------------------------------------------------------- route ----
+// Top-k of one token's E logits by one warp (lane j < k returns the j-th choice):
+// descending logit, ties to the lower expert index (orc_topk).  Each lane holds
+// PER >= ceil(E / 32) candidates (expert lane + 32 i) in registers.
+template <int PER>
+__device__ __forceinline__ int topk_warp(const float* l, int E, int k, int lane) {
+    float v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) v[i] = lane + 32 * i < E ? l[lane + 32 * i] : -INFINITY;
+    unsigned taken = 0;  // bit i: slot i already chosen
+    int my_id = -1;
+    for (int j = 0; j < k; ++j) {
+        float bv = -INFINITY;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = lane + 32 * i;
+            if (e < E && !(taken >> i & 1u) && (v[i] > bv || (v[i] == bv && e < bi))) {
+                bv = v[i];
+                bi = e;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == j) my_id = bi;
+    }
+    return my_id;
+}
+
 // One warp per token: choose k experts, then softmax over their logits.
 //   GATE     : top-k by descending logit, ties to the lower index (orc_topk)
 //   BALANCED : id[t*k+j] = (t*k+j) mod E (exact capacity, workload.cpp:180-195)
@@ -118,32 +151,9 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
     const float* l = c.logits + size_t(t) * c.E;
     int my_id = -1;  // lane j < k holds the j-th chosen expert
     if (c.routing == PERSEUS_ROUTE_GATE) {
-        constexpr int kMaxPer = 32;  // E <= 1024
-        float v[kMaxPer];
         const int per = (c.E + 31) / 32;
-#pragma unroll
-        for (int i = 0; i < kMaxPer; ++i) v[i] = (i < per && lane + 32 * i < c.E) ? l[lane + 32 * i] : -INFINITY;
-        unsigned taken = 0;  // bit i: slot i already chosen
-        for (int j = 0; j < c.k; ++j) {
-            float bv = -INFINITY;
-            int bi = 0x7fffffff;
-#pragma unroll
-            for (int i = 0; i < kMaxPer; ++i) {
-                const int e = lane + 32 * i;
-                if (i < per && e < c.E && !(taken >> i & 1u) && (v[i] > bv || (v[i] == bv && e < bi))) {
-                    bv = v[i];
-                    bi = e;
-                }
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-            }
-            if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-            if (lane == j) my_id = bi;
-        }
+        my_id = per <= 4 ? topk_warp<4>(l, c.E, c.k, lane) : per <= 8 ? topk_warp<8>(l, c.E, c.k, lane)
+                                                                     : topk_warp<32>(l, c.E, c.k, lane);
     } else if (lane < c.k) {
         const int64_t flat = int64_t(t) * c.k + lane;
         my_id = c.routing == PERSEUS_ROUTE_BALANCED ? int(flat % c.E) : c.zipf_ids[flat];
