@@ -188,6 +188,19 @@ def cfg_name(cfg):
     return "custom"
 
 
+def arm_config(args, world, E, mode_name):
+    """The workload description both arms print (same keys, same values)."""
+    c = CONFIGS[args.config]
+    H, I, k, S = c["H"], c["I"], c["k"], args.tokens
+    return {"workload": f"{args.config} MoE layer forward, S={S} tokens/GPU, EP={world} "
+                        f"(ClusterConfig{{{world},1,1}}), {args.routing} routing, {mode_name} signalling",
+            "model": f"{args.config}-moe-layer", "hidden": H, "ffn": I, "experts": E, "top_k": k,
+            "tokens_per_gpu": S, "global_batch": S * world, "seq_len": S,
+            "parallelism": f"ep{world}",
+            "l2": f"inputs > L2: {E // world * 3 * H * I * 2 / 1e9:.2f} GB expert weights + "
+                  f"{S * H * 2 / 1e6:.0f} MB tokens streamed per step"}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -203,7 +216,8 @@ def run_reference_arm(args):
     import math
     q = cfg["E"] // math.gcd(cfg["E"], cfg["k"])  # balanced routing needs E | S*k (workload.cpp:165-168)
     tokens = int((args.ref_budget_s / max(1, args.steps) - fixed) / per_token) // q * q
-    tokens = max(q, min(args.ref_tokens // q * q, tokens))
+    # the full per-GPU workload (S tokens) per step whenever it fits the budget
+    tokens = max(q, min((args.ref_tokens or args.tokens) // q * q, tokens))
     for _ in range(args.warmup if args.warmup < 1 else 1):
         cpu_layer_sample(cfg, tokens)
     vals = []
@@ -219,8 +233,12 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} MoE layer, {tokens} tokens sample per step (CPU)",
-                   "tokens_per_step": tokens},
+        "config": (arm_config(args, args.gpus, cfg["E"], {"combined": "combined", "vanilla": "vanilla",
+                                                           "decoupled": "decoupled"}[args.signaling])
+                   if tokens == args.tokens else
+                   {"workload": f"{args.config} MoE layer, {tokens} tokens sample per step (CPU)",
+                    "tokens_per_step": tokens}),
+        "reference_step": f"one PE's {tokens} tokens per step on the host CPU (the GPU arm: {args.tokens} per GPU)",
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -245,8 +263,8 @@ def main():
                     help="decoupled signal group size (0 = per destination PE, -1 = auto)")
     ap.add_argument("--routing", default="balanced", choices=["balanced", "zipf", "gate"])
     ap.add_argument("--skew", type=float, default=0.0)
-    ap.add_argument("--ref-tokens", type=int, default=1024, help="max tokens per reference-arm step")
-    ap.add_argument("--ref-budget-s", type=float, default=90.0, help="reference arm: target seconds for all steps")
+    ap.add_argument("--ref-tokens", type=int, default=0, help="max tokens per reference-arm step (0 = S)")
+    ap.add_argument("--ref-budget-s", type=float, default=120.0, help="reference arm: target seconds for all steps")
     ap.add_argument("--cpu-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="stage kernels instead of the fused persistent kernel")
@@ -657,14 +675,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "latency_us": ms_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
-            "config": {"workload": f"{args.config} MoE layer forward, S={S} tokens/GPU, EP={world} "
-                                   f"(ClusterConfig{{{world},1,1}}), {args.routing} routing, "
-                                   f"{proto.mode_name()} signalling",
-                       "model": f"{args.config}-moe-layer", "hidden": H, "ffn": I, "experts": E, "top_k": k,
-                       "tokens_per_gpu": S, "global_batch": S * world, "seq_len": S,
-                       "parallelism": f"ep{world}",
-                       "l2": f"inputs > L2: {E // world * 3 * H * I * 2 / 1e9:.2f} GB expert weights + "
-                             f"{S * H * 2 / 1e6:.0f} MB tokens streamed per step"},
+            "config": arm_config(args, world, E, proto.mode_name()),
             "stage_ms": dict(zip(["route_permute", "plan_dispatch", "gemm1_swiglu", "gemm2_combine_put",
                                   "combine"] if args.unfused else
                                  ["route_permute", "plan", "fused_dispatch_ffn_combineput", "-", "combine"],
