@@ -107,9 +107,10 @@ uint64_t perseus_fnv1a64(const void* data, size_t len, uint64_t h);
  *               group's signals (protocols.cpp:250-292); group_size 0 = per PE
  *   NONE      — fault injection: fences suppressed (transport.cpp:104-106)
  *   FAULT_EARLY — fault injection: every dispatch flag is written when its
- *               tile's put is ISSUED (before the data), no fence — the
- *               "signal before data" bug the ordering checker must catch
- *               (verify_ordering, metrics.cpp:118-138) */
+ *               tile's put is ISSUED (before the data, which then trails by
+ *               200 us as on a congested link), no fence — the "signal before
+ *               data" bug the ordering checker must catch (verify_ordering,
+ *               metrics.cpp:118-138) */
 #define PERSEUS_SIGNAL_COUPLED 0
 #define PERSEUS_SIGNAL_DECOUPLED 1
 #define PERSEUS_SIGNAL_NONE 2

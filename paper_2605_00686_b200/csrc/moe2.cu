@@ -517,6 +517,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 if (c.trace) trace_ev(c, PERSEUS_EV_DISPATCH_SIGNAL, st.dst, st.tile_id, st.group, 0, 0, fwd_now());
             }
         }
+        // (fault) ... and the remote puts are slow to land (a congested link): they
+        // start 200 us after their signals — later than the receivers reach their
+        // first remote tiles — so receivers that trust the flags read rows not there yet
+        const uint64_t t_fault = globaltimer() + 200000;
         while (true) {
             const bool remote_q = state == 1;
             int u = 0;
@@ -551,6 +555,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (r0 >= st.rows) continue;
             const int nrows = min(kUnitRows, st.rows - r0);
             if (remote_q && first_remote) {
+                if (c.signaling == PERSEUS_SIGNAL_FAULT_EARLY)
+                    while (globaltimer() < t_fault) __nanosleep(1000);
                 if (lane == 0) atomicMin(c.fwd_t + kFwdDispFirst, fwd_now());
                 first_remote = false;
             }

@@ -136,11 +136,11 @@ def main():
                 ok = False
                 entry["ok"] = False
             if proto.fault_early_signal:
-                # reported, not required here: across GPUs the dispatch (~600 GB/s) outruns the
-                # receivers' consumption of remote tiles, so an early flag is rarely first seen
-                # before its rows land; the one-GPU concurrent test (tests/test_gpu_concurrent.py)
-                # is where the checker is required to fire
+                # the checker must catch the signal-before-data fault in every forward
                 entry["caught_fraction"] = sum(1 for v in viol if v > 0) / len(viol)
+                if entry["caught_fraction"] < 1.0:
+                    ok = False
+                    entry["ok"] = False
             traces.append(entry)
     if rank == 0:
         verdict = ok and all(rr["ok"] for res in results for rr in res)

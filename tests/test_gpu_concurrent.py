@@ -164,7 +164,8 @@ def test_concurrent_device_trace_safe_protocols(oracle, P, proto):
 @pytest.mark.parametrize("P", [2, 4])
 def test_fault_signal_before_data_is_caught(oracle, P):
     """Fault injection (PERSEUS_SIGNAL_FAULT_EARLY): every dispatch flag is
-    written when its tile's put is issued, before the rows, without a fence.
+    written when its tile's put is issued, before the rows (which trail by 200 us),
+    without a fence.
     The receivers' first-observation content checks must report it as ordering
     violations (verify_ordering) in >= 99% of trials — here in every one."""
     pb = _pb()
