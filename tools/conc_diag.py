@@ -1,5 +1,10 @@
-"""Diagnostics: P ranks concurrently on one GPU (tests/gpu_util.run_concurrent),
-per-rank counters + kernel timelines, for a few grid caps."""
+"""Diagnostics: P ranks concurrently on one GPU, per-rank counters + kernel
+timelines, for a few grid caps.  Launched WITH programmatic dependent launch
+(unlike tests/gpu_util.run_concurrent, which passes pdl=False) unless
+DIAG_NO_PDL=1: with PDL a rank's grid waiting for its primary holds up the work
+distributor and another rank's fused kernel stays unscheduled until the signal
+waits time out (timeouts per rank in the output).
+    python tools/conc_diag.py P CAP[,CAP...] ITERS TIMELINE(0|1|2)"""
 import json
 import os
 import sys
@@ -20,7 +25,8 @@ m = pb.ModelConfig("qwen3", 2048, 768, 96 if P == 3 else 128, 8)
 for cap in caps:
     os.environ["PERSEUS_NUM_SMS"] = str(cap)
     layers = [pb.MoELayer(m, S, rank=r, world=P, device=0, routing="balanced", seed=3,
-                          protocol=(pb.decoupled_protocol(0) if os.environ.get("DIAG_PROTO") == "decoupled" else pb.combined_protocol(0)), pair=os.environ.get("DIAG_PAIR", "1") == "1")
+                          protocol=(pb.decoupled_protocol(0) if os.environ.get("DIAG_PROTO") == "decoupled" else pb.combined_protocol(0)), pair=os.environ.get("DIAG_PAIR", "1") == "1",
+                          pdl=os.environ.get("DIAG_NO_PDL", "0") != "1")
               for r in range(P)]
     pb.MoELayer.connect_local(layers)
     xs = [torch.empty(S, 2048, dtype=torch.bfloat16, device="cuda") for _ in range(P)]
