@@ -175,3 +175,24 @@ def test_fault_signal_before_data_is_caught(oracle, P):
     caught = sum(1 for rep, _, _ in reps if rep["dispatch"]["ordering_violations"] > 0)
     viol = [rep["dispatch"]["ordering_violations"] for rep, _, _ in reps]
     assert caught >= 0.99 * trials, viol
+
+
+@pytest.mark.parametrize("P,S,E,k,routing", [
+    (1, 1, 8, 2, "gate"),        # a single token
+    (2, 3, 16, 2, "gate"),       # a few tokens: most (src, expert) transfers are empty and omitted
+    (2, 64, 256, 16, "gate"),    # the largest expert count / top-k the layer accepts
+    (4, 40, 64, 8, "zipf"),      # Zipf 2.0: many zero-row experts, one hot expert
+])
+def test_edge_sizes_concurrent(oracle, P, S, E, k, routing):
+    """Edge cases the reference's tests cover for its layout (zero-size transfers
+    omitted, workload.cpp:135; ragged tiles) through the production fused kernel:
+    1-token and few-token batches, E = 256 / top-16, heavy Zipf skew."""
+    from tests.gpu_util import run_concurrent
+    pb = _pb()
+    m = pb.ModelConfig("edge", 512, 256, E, k)
+    skew = 2.0 if routing == "zipf" else 0.0
+    protocol = pb.combined_protocol(0)
+    layers, xs, outs = run_concurrent(pb, m, S, P, routing=routing, skew=skew, seed=21, protocol=protocol, reps=2)
+    _check_all(oracle, pb, m, S, P, layers, xs, outs, routing, 21, skew, protocol, 2)
+    for l in layers:
+        l.close()
