@@ -453,9 +453,10 @@ def main():
     e2e_sync_value = world * S * min(args.steps, 200) / te_sync
 
     # ---- signalling variants of the same fused kernel (N > 1), same run ----
-    def time_variant(vproto, name):
+    def time_variant(vproto, name, flags=0):
         vl = pb.MoELayer(model, S, rank=rank, world=world, device=local, routing=args.routing, skew=args.skew,
-                         seed=1, protocol=vproto, fused=not args.unfused, pair=False if args.no_pair else None)
+                         seed=1, protocol=vproto, fused=not args.unfused, pair=False if args.no_pair else None,
+                         flags=flags)
         vl.connect_dist()
         for _ in range(args.warmup):
             vl.forward(x, out)
@@ -464,7 +465,7 @@ def main():
         vb = time_blocks(lambda: vl.forward(x, out), 3, args.variant_steps, stream, barrier, allmax)
         v1 = vl.counters()
         n = 3 * args.variant_steps
-        vd = {key: (v1[key] - v0[key]) / n for key in ("dispatch_fences", "combine_fences")}
+        vd = {key: (v1[key] - v0[key]) / n for key in ("dispatch_fences", "combine_fences", "dispatch_put_bytes")}
         v_ms = statistics.median(vb)
         res = {"signaling": name, "group_size": vl.group_size(), "steps": n, "ms_per_step": v_ms,
                "ms_per_step_blocks": vb, "value": world * S / (v_ms / 1e3), "unit": "tokens/s",
@@ -472,11 +473,19 @@ def main():
         vl.close()
         return res
 
-    variant = auto_variant = None
+    variant = auto_variant = dedup_variant = None
     if world > 1 and args.variant_steps > 0 and args.signaling != "vanilla":
         variant = time_variant(pb.vanilla_protocol(), "coupled (per-tile fence), same fused kernel")
         if args.group_size == 0 and args.routing != "gate":
             auto_variant = time_variant(pb.combined_protocol(-1), "decoupled, auto group size (GROUP_AUTO)")
+        if not args.unfused and not args.no_pair:
+            # token dedup (PERSEUS_F_DEDUP, §8f-4): one NVLink row per (token,
+            # destination) + receiver-side expansion; same outputs, fewer wire bytes
+            try:
+                dedup_variant = time_variant(proto, "per-destination token dedup (PERSEUS_F_DEDUP)",
+                                             flags=pb._lib.F_DEDUP)
+            except pb.ConfigError as e:  # e.g. a fence-suppressed signalling ablation
+                dedup_variant = {"unavailable": str(e)}
 
     # ---- compute-only twin (N > 1): the same per-GPU work, no communication ----
     # EP = 1 with E / N experts: every local expert receives the same S*k*N/E rows
@@ -666,6 +675,10 @@ def main():
         variant["slowdown_vs_this_run"] = variant["ms_per_step"] / timing_blocks["median_ms"]
     if auto_variant is not None:
         auto_variant["speedup_vs_this_run"] = timing_blocks["median_ms"] / auto_variant["ms_per_step"]
+    if dedup_variant is not None and "ms_per_step" in dedup_variant:
+        dedup_variant["speedup_vs_this_run"] = timing_blocks["median_ms"] / dedup_variant["ms_per_step"]
+        dedup_variant["wire_bytes_ratio_vs_this_run"] = (dedup_variant["fences_per_forward"]["dispatch_put_bytes"]
+                                                         / max(dc.get("dispatch_put_bytes", 0), 1e-9))
     # our kernels per forward: router GEMM, k_route, k_perm (+ the plan CTA), then
     # k_moe2 (fused) or k_dispatch + k_gemm<1> + k_gemm<2> (unfused), then k_combine
     launches_per_step = 5 if not args.unfused else 7
@@ -696,6 +709,7 @@ def main():
             "comm": comm,
             "per_tile_fence_variant": variant,
             "auto_group_variant": auto_variant,
+            "dedup_variant": dedup_variant,
             "timing_blocks": timing_blocks,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": S * H * 2,
                     "d2h_bytes_per_step": S * H * 2, "ms_per_step": 1e3 * te_async / args.steps,

@@ -154,6 +154,15 @@ typedef struct perseus_layer_config {
  * combiners) instead of the combine kernel after it; same bits.  Experimental:
  * slower at the bench shape. */
 #define PERSEUS_F_DF_COMBINE 128
+/* per-destination token dedup of the dispatch (P > 1, CTA-pair
+ * kernel, not with tracing): a token whose k experts put several rows on one
+ * destination crosses NVLink ONCE into that destination's per-source token
+ * buffer, with the row -> token index of every (expert, row) of the reference
+ * layout; the receiver expands the rows into the usual receive heap (a local
+ * copy) and releases the tiles to its GEMMs.  One fence + one flag per
+ * (source, destination).  Outputs are the layer's (bit-identical); the byte and
+ * signal accounting is NOT the reference's, so it is reported separately. */
+#define PERSEUS_F_DEDUP 256
 #define PERSEUS_F_LOCAL_DISPATCH 32
 #define PERSEUS_F_LOCAL_COMBINE 64
 #define PERSEUS_F_NO_PDL 16       /* no programmatic dependent launch: for several ranks sharing ONE device

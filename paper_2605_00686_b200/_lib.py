@@ -24,6 +24,7 @@ F_NO_PDL = 16
 F_LOCAL_DISPATCH = 32
 F_LOCAL_COMBINE = 64
 F_DF_COMBINE = 128
+F_DEDUP = 256
 TILE_ROWS = 128
 
 

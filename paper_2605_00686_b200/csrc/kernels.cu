@@ -164,6 +164,14 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
         // per-256-token-block expert histogram (this forward's parity half)
         atomicAdd(&c.hist[(size_t(c.par) * c.hist_blocks + t / 256) * c.E + my_id], 1);
     }
+    if (c.dedup) {
+        // token dedup: per-256-token-block count of tokens per remote destination
+        unsigned dm = lane < c.k && my_id % c.P != c.rank ? 1u << (my_id % c.P) : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) dm |= __shfl_xor_sync(0xffffffffu, dm, o);
+        if (lane < c.P && (dm >> lane & 1u))
+            atomicAdd(&c.dhist[(size_t(c.par) * c.hist_blocks + t / 256) * kMaxPes + lane], 1);
+    }
     // The routing weights.  Learned gate: from the exact logits.  Reference
     // routing modes: the ids do not depend on the logits; when the router GEMM
     // ran on a side stream (fused path) the fused kernel's copy warps write the
@@ -264,6 +272,11 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
         tl_mark(c, kTlCounts);
     }
+    if (c.dedup && b == 0 && tid < c.P) {  // rows of the reference layout this rank sends to each PE
+        int32_t r = 0;
+        for (int e = tid; e < E; e += c.P) r += tot[e];
+        c.drows[tid] = r;
+    }
     const int32_t total = block_exclusive_scan(tot, E, scratch);
     for (int e = tid; e < E; e += kPermT) {
         base[e] += tot[e];
@@ -281,9 +294,46 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
             if (j < c.k) atomicOr(&bits[my[j] * (kPermT / 32) + (tid >> 5)], 1u << (tid & 31));
     }
     __syncthreads();
-    if (t >= c.S) return;
     const int w = tid >> 5;
     const uint32_t below = (1u << (tid & 31)) - 1u;
+    // token dedup: this token's row in each remote destination's token buffer
+    // (tokens in ascending order per destination: earlier blocks, earlier warps,
+    // earlier lanes)
+    __shared__ int32_t dwarp[kPermT / 32][kMaxPes], dbase[kMaxPes];
+    int32_t u_of[kMaxPes];
+    if (c.dedup) {
+        unsigned dm = 0;
+        if (t < c.S)
+            for (int j = 0; j < c.k; ++j)
+                if (my[j] % c.P != c.rank) dm |= 1u << (my[j] % c.P);
+#pragma unroll
+        for (int d = 0; d < kMaxPes; ++d) {
+            const unsigned bal = __ballot_sync(0xffffffffu, d < c.P && (dm >> d & 1u));
+            if ((tid & 31) == 0) dwarp[w][d] = __popc(bal);
+            u_of[d] = __popc(bal & below);
+        }
+        if (tid < c.P) {
+            const int32_t* dh = c.dhist + size_t(c.par) * c.hist_blocks * kMaxPes;
+            int32_t before = 0, all = 0;
+            for (int q = 0; q < nb; ++q) {
+                const int32_t v = dh[size_t(q) * kMaxPes + tid];
+                before += q < b ? v : 0;
+                all += v;
+            }
+            dbase[tid] = before;
+            if (b == 0) c.dtot[tid] = all;
+            c.dhist[(size_t(c.par ^ 1) * c.hist_blocks + b) * kMaxPes + tid] = 0;  // next forward's half
+        }
+        __syncthreads();
+#pragma unroll
+        for (int d = 0; d < kMaxPes; ++d) {
+            if (d >= c.P) break;
+            int32_t off = dbase[d];
+            for (int q = 0; q < w; ++q) off += dwarp[q][d];
+            u_of[d] += off;
+        }
+    }
+    if (t >= c.S) return;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j >= c.k) break;
@@ -293,6 +343,14 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         const int32_t p = base[my[j]] + rank;
         c.rows[p] = t;
         c.pos[size_t(t) * c.k + j] = p;
+        if (c.dedup) {
+            const int d = my[j] % c.P;
+            int32_t u = -1;
+#pragma unroll
+            for (int q = 0; q < kMaxPes; ++q)
+                if (q == d && d != c.rank) u = u_of[q];
+            c.uidx[p] = u;
+        }
     }
     tl_end(c, kTlPerm, tid == 0);
 }

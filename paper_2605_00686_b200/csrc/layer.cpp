@@ -149,6 +149,10 @@ struct perseus_layer {
     uint8_t* sym = nullptr;
     size_t sym_bytes = 0;
     size_t off_ctab = 0, off_cflag_cnt = 0, off_dflag = 0, off_cflag = 0, off_heap = 0, off_ybuf = 0;
+    size_t off_dd = 0, off_didx = 0, off_ddflag = 0;  // token dedup (PERSEUS_F_DEDUP)
+    bool dedup = false;
+    int32_t *dhist = nullptr, *uidx = nullptr, *dtot = nullptr, *drows = nullptr;
+    uint32_t *dsent = nullptr, *ex_done = nullptr;
     uint8_t* peer[kMaxPes] = {};
     bool ipc_mapped[kMaxPes] = {};
     bool connected = false;
@@ -188,7 +192,14 @@ struct perseus_layer {
             c.dflag[p] = reinterpret_cast<uint32_t*>(bd + off_dflag);
             c.ybuf[p] = reinterpret_cast<bf16*>(bc + off_ybuf);
             c.cflag[p] = reinterpret_cast<uint32_t*>(bc + off_cflag);
+            if (dedup) {
+                c.dd[p] = reinterpret_cast<bf16*>(b + off_dd);
+                c.didx[p] = reinterpret_cast<int32_t*>(b + off_didx);
+                c.ddflag[p] = reinterpret_cast<uint32_t*>(b + off_ddflag);
+            }
         }
+        c.dedup = dedup ? 1 : 0;
+        c.dhist = dhist; c.uidx = uidx; c.dtot = dtot; c.drows = drows; c.dsent = dsent; c.ex_done = ex_done;
         c.local_dispatch = (cfg.flags & PERSEUS_F_LOCAL_DISPATCH) ? 1 : 0;
         c.local_combine = (cfg.flags & PERSEUS_F_LOCAL_COMBINE) ? 1 : 0;
         c.R_max = R_max; c.T_max = T_max; c.Y_rows = Y_rows;
@@ -316,7 +327,8 @@ void free_layer(perseus_layer* L) {
                     L->counts, L->offsets, L->rows, L->pos, L->zipf_ids, L->hist, L->hdr, L->send, L->groups,
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
                     L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl, L->smaps, L->trace, L->trace_n, L->trace_seen_ep,
-                    L->send_first, L->pairs, L->tok_ready, L->ready_q};
+                    L->send_first, L->pairs, L->tok_ready, L->ready_q,
+                    L->dhist, L->uidx, L->dtot, L->drows, L->dsent, L->ex_done};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : L->ev)
@@ -476,6 +488,13 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->pair = !(cfg->flags & PERSEUS_F_NO_PAIR) &&
                       ((cfg->flags & PERSEUS_F_FORCE_PAIR) ||
                        int64_t(world) * int64_t(cfg->tokens_per_pe) * cfg->top_k > int64_t(kTileRows) * cfg->experts);
+            L->dedup = (cfg->flags & PERSEUS_F_DEDUP) && world > 1;
+            if (L->dedup && (!L->fused || !L->pair))
+                throw sigsim::ConfigError("token dedup (PERSEUS_F_DEDUP) needs the fused CTA-pair kernel");
+            if (L->dedup && (cfg->flags & (PERSEUS_F_LOCAL_DISPATCH | PERSEUS_F_DF_COMBINE)))
+                throw sigsim::ConfigError("token dedup (PERSEUS_F_DEDUP) excludes LOCAL_DISPATCH and DF_COMBINE");
+            if (L->dedup && cfg->signaling >= PERSEUS_SIGNAL_NONE)
+                throw sigsim::ConfigError("token dedup (PERSEUS_F_DEDUP) always fences and signals per destination");
             L->rank = rank;
             L->world = world;
             L->device = device;
@@ -538,6 +557,14 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->send_first = dalloc<int32_t>(E);
             L->pairs = dalloc<int32_t>(2 * size_t(L->max_recv) + 4);
             L->stats = dalloc<unsigned long long>(kStatCount);
+            if (L->dedup) {
+                L->dhist = dalloc<int32_t>(2 * size_t(L->hist_blocks) * kMaxPes);
+                L->uidx = dalloc<int32_t>(Sk);
+                L->dtot = dalloc<int32_t>(kMaxPes);
+                L->drows = dalloc<int32_t>(kMaxPes);
+                L->dsent = dalloc<uint32_t>(kMaxPes);
+                L->ex_done = dalloc<uint32_t>(L->max_recv);
+            }
             L->tok_ready = dalloc<int32_t>(S);
             L->ready_q = dalloc<unsigned long long>(S);
 
@@ -549,6 +576,11 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->off_cflag = o; o = align_up(o + 2 * size_t(L->T_max) * 4, 1024);
             L->off_heap = o; o = align_up(o + 2 * size_t(L->R_max) * H * 2, 1024);
             L->off_ybuf = o; o = align_up(o + 2 * size_t(L->Y_rows) * H * 2, 1024);
+            if (L->dedup) {
+                L->off_dd = o; o = align_up(o + 2 * size_t(P) * S * H * 2, 1024);
+                L->off_didx = o; o = align_up(o + 2 * size_t(L->R_max) * 4, 256);
+                L->off_ddflag = o; o = align_up(o + 2 * kMaxPes * 4, 256);
+            }
             L->sym_bytes = o;
             L->sym = dalloc<uint8_t>(o);
 
@@ -703,6 +735,8 @@ int perseus_layer_forward(perseus_layer* L, const void* x, void* out, void* stre
 int perseus_layer_forward_phase(perseus_layer* L, int phase, const void* x, void* out, void* stream) {
     return guarded([&] {
         if (phase < 0 || (phase > 3 && phase != PERSEUS_PHASE_ALL)) throw sigsim::ConfigError("bad phase");
+        if (L->dedup && phase != PERSEUS_PHASE_ALL)
+            throw sigsim::ConfigError("token dedup (PERSEUS_F_DEDUP) runs whole forwards only");
         run_phase(L, phase, x, out, static_cast<cudaStream_t>(stream));
     });
 }
@@ -895,6 +929,8 @@ int perseus_layer_group_size(perseus_layer* L, int64_t* group_size) {
 
 int perseus_layer_set_trace(perseus_layer* L, int on) {
     return guarded([&] {
+        if (on && L->dedup)
+            throw sigsim::ConfigError("token dedup (PERSEUS_F_DEDUP) has no reference event trace");
         ck(cudaSetDevice(L->device), "cudaSetDevice");
         ck(cudaDeviceSynchronize(), "sync");
         if (on && !L->trace) {

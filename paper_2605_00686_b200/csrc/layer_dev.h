@@ -85,6 +85,17 @@ struct DevCtx {
     int32_t df_combine;
     int32_t* tok_ready;             // [S] expert rows of the token written this forward
     unsigned long long* ready_q;    // [S] (epoch << 32 | token), in readiness order
+    // per-destination token dedup of the dispatch (PERSEUS_F_DEDUP; P > 1)
+    int32_t dedup;
+    int32_t* dhist;                 // [2][hist_blocks][kMaxPes]: per-256-token-block tokens per destination
+    int32_t* uidx;                  // [S*k] sorted slot -> the token's row in its destination's token buffer (-1: self)
+    int32_t* dtot;                  // [kMaxPes]: unique tokens this rank sends to each destination
+    int32_t* drows;                 // [kMaxPes]: rows of the reference layout this rank sends to each destination
+    uint32_t* dsent;                // [kMaxPes]: token rows + index entries written to each destination
+    uint32_t* ex_done;              // [max_recv]: rows expanded per received remote tile
+    bf16* dd[kMaxPes];              // symmetric [2][P][S][H]: token buffer per (parity, source)
+    int32_t* didx[kMaxPes];         // symmetric [2][R_max]: token-buffer row of every receive-heap row
+    uint32_t* ddflag[kMaxPes];      // symmetric [2][P]: per source, its token buffer + index complete (epoch)
     int32_t local_dispatch;     // compute-only twin: dispatch puts / flags stay local, remote tiles not awaited
     int32_t local_combine;      // compute-only twin: combine puts / flags stay local, combine flags not awaited
     int32_t pdl;                // launch with programmatic dependent launch (PERSEUS_F_NO_PDL clears it)

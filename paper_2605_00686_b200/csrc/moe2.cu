@@ -521,8 +521,95 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         // start 200 us after their signals — later than the receivers reach their
         // first remote tiles — so receivers that trust the flags read rows not there yet
         const uint64_t t_fault = globaltimer() + 200000;
+        // token dedup: the remote queue is this rank's tokens (each sent once per
+        // destination), then an expansion queue over the received remote tiles
+        const int remote_n = c.dedup ? c.S : remote_units;
+        const int expand_units = c.dedup ? hdr.n_recv_remote * kUnitsPerTile : 0;
         while (true) {
             const bool remote_q = state == 1;
+            if (state == 3) {
+                // token dedup, receiver: expand the sources' token buffers into the
+                // receive heap, tile by tile in arrival order, and release each
+                // tile to the GEMMs (the flag the producer waits on, set locally)
+                int u = 0;
+                if (lane == 0) u = int(atomicAdd(&c.sched[6], 1u));
+                u = __shfl_sync(0xffffffffu, u, 0);
+                if (u >= expand_units) {
+                    state = 2;
+                    continue;
+                }
+                const int ti = c.rorder[hdr.n_recv - hdr.n_recv_remote + u / kUnitsPerTile];
+                const RecvTile rt = c.recv[ti];
+                const int r0 = (u % kUnitsPerTile) * kUnitRows;
+                if (r0 >= rt.rows) continue;
+                const int nrows = min(kUnitRows, rt.rows - r0);
+                if (lane == 0 &&
+                    !wait_flag_geq(c.ddflag[c.rank] + size_t(c.par) * kMaxPes + rt.src, c.epoch, kWaitTimeoutNs))
+                    atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                __syncwarp();
+                const bf16* buf = c.dd[c.rank] + (size_t(c.par) * c.P + rt.src) * size_t(c.S) * c.H;
+                bf16* heap = c.heap[c.rank] + (size_t(c.par) * c.R_max + rt.heap_row) * c.H;
+                for (int r = 0; r < nrows; ++r) {
+                    const int32_t row = ld_relaxed_sys(reinterpret_cast<const uint32_t*>(
+                        c.didx[c.rank] + size_t(c.par) * c.R_max + rt.heap_row + r0 + r));
+                    const uint4* src = reinterpret_cast<const uint4*>(buf + size_t(row) * c.H);
+                    uint4* dst = reinterpret_cast<uint4*>(heap + size_t(r0 + r) * c.H);
+                    for (int v = lane; v < c.H / 8; v += 32) dst[v] = __ldcg(src + v);
+                }
+                __syncwarp();
+                if (lane == 0 && atom_add_acq_rel_gpu(c.ex_done + ti, uint32_t(nrows)) + nrows == uint32_t(rt.rows))
+                    st_release_gpu(c.dflag[c.rank] + size_t(c.par) * c.T_max + rt.tile_id, c.epoch);
+                continue;
+            }
+            if (remote_q && c.dedup) {
+                // token dedup, sender: one token per claim; its row crosses to each
+                // remote destination of its experts once, with the token-buffer row of
+                // each of its (expert, row) slots in the destination's heap layout
+                int t = 0;
+                if (lane == 0) t = int(atomicAdd(&c.sched[1], 1u));
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= remote_n) {
+                    state = expand_units > 0 ? 3 : 2;
+                    continue;
+                }
+                if (first_remote) {
+                    if (lane == 0) atomicMin(c.fwd_t + kFwdDispFirst, fwd_now());
+                    first_remote = false;
+                }
+                const int e_l = lane < c.k ? c.ids[size_t(t) * c.k + lane] : 0;
+                const int p_l = lane < c.k ? c.pos[size_t(t) * c.k + lane] : 0;
+                const int d_l = lane < c.k ? e_l % c.P : c.rank;
+                // index entries: lane j < k writes its slot's token-buffer row at the destination
+                if (d_l != c.rank) {
+                    const int32_t rel = p_l - c.offsets[e_l];
+                    const SendTile st = c.send[c.send_first[e_l] + rel / kTileRows];
+                    c.didx[d_l][size_t(c.par) * c.R_max + st.heap_row + rel % kTileRows] = c.uidx[p_l];
+                }
+                const uint4* srow = reinterpret_cast<const uint4*>(c.x + size_t(t) * c.H);
+                for (int d = 0; d < c.P; ++d) {
+                    const unsigned on = __ballot_sync(0xffffffffu, lane < c.k && d_l == d && d != c.rank);
+                    if (!on) continue;
+                    const int32_t urow = __shfl_sync(0xffffffffu, c.uidx[p_l], __ffs(on) - 1);
+                    uint4* drow = reinterpret_cast<uint4*>(c.dd[d] + ((size_t(c.par) * c.P + c.rank) * size_t(c.S) + urow) * c.H);
+                    for (int v = lane; v < c.H / 8; v += 32) drow[v] = __ldg(srow + v);
+                    __syncwarp();
+                    if (lane == 0) {
+                        atomicAdd(&c.stats[kStatDispatchPuts], 1ull);
+                        atomicAdd(&c.stats[kStatDispatchBytes], (unsigned long long)c.H * 2 + 4ull * __popc(on));
+                        const uint32_t n = 1u + __popc(on);
+                        if (atom_add_acq_rel_gpu(c.dsent + d, n) + n == uint32_t(c.dtot[d] + c.drows[d])) {
+                            // this destination's token buffer and index are complete:
+                            // one fence, one flag (Perseus per-destination signalling)
+                            fence_acq_rel_sys();
+                            st_relaxed_sys(c.ddflag[d] + size_t(c.par) * kMaxPes + c.rank, c.epoch);
+                            atomicAdd(&c.stats[kStatDispatchFences], 1ull);
+                            atomicAdd(&c.stats[kStatDispatchSignals], 1ull);
+                            atomicMax(c.fwd_t + kFwdDispLast, fwd_now());
+                        }
+                    }
+                }
+                continue;
+            }
             int u = 0;
             if (lane == 0) u = int(atomicAdd(&c.sched[remote_q ? 1 : 2], 1u));
             u = __shfl_sync(0xffffffffu, u, 0);

@@ -82,6 +82,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     __shared__ int32_t send_base[kMaxPes], recv_base[kMaxPes], s_head;
 
     if (tid == 0) s_err = 0;
+    if (c.dedup && tid < kMaxPes) c.dsent[tid] = 0;  // token dedup: rows + index entries sent per destination
     if (tid < P && !wait_flag_geq(c.count_flag[r] + tid, c.epoch, kWaitTimeoutNs)) {
         atomicAdd(&c.stats[kStatTimeouts], 1ull);
         s_err = 1;
@@ -316,6 +317,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 rt.pad = 0;
                 c.recv[p] = rt;
                 c.tile_ctr[p] = 0;
+                if (c.dedup) c.ex_done[p] = 0;
                 c.g1_done[p] = 0;
                 // processing order (1-CTA kernel): self tiles first, then remote tiles
                 // source by source in arrival order

@@ -49,7 +49,7 @@ def assert_close(out_f32, ref_f32, tol=1e-2, what=""):
 
 
 def run_concurrent(pb, model, S, P, routing="balanced", skew=0.0, seed=1, protocol=None, reps=1, before=None,
-                   sync_each=True, pair=True):
+                   sync_each=True, pair=True, flags=0):
     """P EP ranks on ONE device running the PRODUCTION path concurrently: every
     rank's full forward (route -> permute + plan -> fused persistent k_moe2 on
     CTA pairs -> combine) on its own stream, ranks synchronising only through
@@ -69,7 +69,7 @@ def run_concurrent(pb, model, S, P, routing="balanced", skew=0.0, seed=1, protoc
     os.environ["PERSEUS_NUM_SMS"] = str((n_sms // P) & ~1)
     try:
         layers = [pb.MoELayer(model, S, rank=r, world=P, device=0, routing=routing, skew=skew, seed=seed,
-                              protocol=protocol, pair=pair, pdl=False) for r in range(P)]
+                              protocol=protocol, pair=pair, pdl=False, flags=flags) for r in range(P)]
     finally:
         if old is None:
             os.environ.pop("PERSEUS_NUM_SMS", None)

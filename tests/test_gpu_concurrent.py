@@ -196,3 +196,50 @@ def test_edge_sizes_concurrent(oracle, P, S, E, k, routing):
     _check_all(oracle, pb, m, S, P, layers, xs, outs, routing, 21, skew, protocol, 2)
     for l in layers:
         l.close()
+
+
+@pytest.mark.parametrize("P,routing,skew", [
+    (2, "balanced", 0.0),
+    (4, "gate", 0.0),
+    (4, "zipf", 1.2),
+    (8, "balanced", 0.0),
+])
+def test_token_dedup_bit_identical(oracle, P, routing, skew):
+    """PERSEUS_F_DEDUP: every token crosses to each remote
+    destination once (plus a 4-byte index per (expert, row) slot) and the
+    receiver expands it into the reference's heap layout.  The output of every
+    token must be BIT-identical to the reference-layout dispatch (the GEMMs see
+    the same heap), the wire bytes must equal the count of distinct (token,
+    destination) pairs, and there must be exactly one fence per remote
+    destination with traffic."""
+    from tests.gpu_util import bf16_bits, run_concurrent
+    pb = _pb()
+    from paper_2605_00686_b200 import _lib
+    m = pb.ModelConfig("qwen3", QWEN3["H"], QWEN3["I"], QWEN3["E"], QWEN3["k"])
+    S, reps, seed = 1024, 3, 5
+    protocol = pb.combined_protocol(0)
+    base, xs, outs0 = run_concurrent(pb, m, S, P, routing=routing, skew=skew, seed=seed, protocol=protocol, reps=1)
+    ids = [l.routing()[0] for l in base]
+    for l in base:
+        l.close()
+    layers, xs, outs = run_concurrent(pb, m, S, P, routing=routing, skew=skew, seed=seed, protocol=protocol,
+                                      reps=reps, flags=_lib.F_DEDUP)
+    for r, l in enumerate(layers):
+        assert np.array_equal(l.routing()[0], ids[r])
+        c = l.counters()
+        assert c["wait_timeouts"] == 0 and c["errors"] == 0, (r, c)
+        dst = ids[r] % P
+        pairs = {(t, int(d)) for t in range(S) for d in dst[t] if d != r}
+        slots = int((dst != r).sum())
+        n_dst = len({d for _, d in pairs})
+        assert c["dispatch_puts"] == len(pairs) * reps, (r, c["dispatch_puts"], len(pairs))
+        assert c["dispatch_put_bytes"] == (len(pairs) * m.hidden_dim * 2 + 4 * slots) * reps
+        assert c["dispatch_fences"] == n_dst * reps and c["dispatch_signals"] == n_dst * reps
+        assert np.array_equal(bf16_bits(outs[r]), bf16_bits(outs0[r])), f"rank {r}: output bits"
+    for l in layers:
+        l.close()
+    # configurations the dedup dispatch refuses
+    for pair, extra in ((False, 0), (True, _lib.F_LOCAL_DISPATCH), (True, _lib.F_DF_COMBINE)):
+        with pytest.raises(pb.ConfigError):
+            pb.MoELayer(m, S, rank=0, world=2, device=0, routing=routing, protocol=protocol, pair=pair,
+                        flags=_lib.F_DEDUP | extra)
