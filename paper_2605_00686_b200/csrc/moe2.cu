@@ -525,6 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         // destination), then an expansion queue over the received remote tiles
         const int remote_n = c.dedup ? c.S : remote_units;
         const int expand_units = c.dedup ? hdr.n_recv_remote * kUnitsPerTile : 0;
+        bool expanded = false;  // this warp found the expansion queue empty
         while (true) {
             const bool remote_q = state == 1;
             if (state == 3) {
@@ -535,7 +536,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 if (lane == 0) u = int(atomicAdd(&c.sched[6], 1u));
                 u = __shfl_sync(0xffffffffu, u, 0);
                 if (u >= expand_units) {
-                    state = 2;
+                    state = expanded ? 4 : 2;  // 4: done (came here from the self rest)
+                    expanded = true;
+                    if (state == 4) break;
                     continue;
                 }
                 const int ti = c.rorder[hdr.n_recv - hdr.n_recv_remote + u / kUnitsPerTile];
@@ -614,6 +617,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (lane == 0) u = int(atomicAdd(&c.sched[remote_q ? 1 : 2], 1u));
             u = __shfl_sync(0xffffffffu, u, 0);
             if (u >= (remote_q ? remote_units : self_units)) {
+                if (state == 2 && expand_units > 0 && !expanded) {
+                    // token dedup: warps done with the self rows help expand
+                    expanded = true;
+                    state = 3;
+                    continue;
+                }
                 if (state == 2) break;
                 state = (state == 0 && remote_ok) ? 1 : 2;
                 continue;

@@ -19,10 +19,13 @@ print(" exposed", json.dumps(c["exposed"]), "ep1 twin", round(c["compute_only_tw
 print(" nvlink alg", json.dumps(c["nvlink_algorithmic_bytes_per_forward"]), "twins", json.dumps({k: v["median_ms"] for k, v in c["same_schedule_twins"].items() if isinstance(v, dict)}))
 print(" per-tile", json.dumps({k: d["per_tile_fence_variant"][k] for k in ("ms_per_step", "fences_per_forward")}))
 print(" auto-gs", json.dumps({k: d["auto_group_variant"][k] for k in ("ms_per_step", "group_size", "fences_per_forward")}) if d["auto_group_variant"] else None)
+dv = d.get("dedup_variant")
+print(" dedup", json.dumps({k: dv.get(k) for k in ("ms_per_step", "speedup_vs_this_run", "wire_bytes_ratio_vs_this_run", "fences_per_forward", "unavailable")}) if dv else None)
 print(" roofline", json.dumps({k: d["roofline"].get(k) for k in ("bound", "frac", "launch_ms")}), json.dumps(d["layer_roofline"]["frac_of_max_compute_nvlink"]))
 PY
 done
 # NCCL all-to-all baseline (bulk synchronous, precomputed splits, CUDA graph) at the same N
+[ -n "$SKIP_NCCL" ] && exit 0
 for N in ${NS:-2 4}; do
   [ $N -le $NG ] || continue
   timeout 120 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2961$N \
