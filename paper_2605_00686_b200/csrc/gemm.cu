@@ -132,6 +132,11 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
     constexpr int kTlId = kMode == 0 ? kTlGate : (kMode == 1 ? kTlGemm1 : kTlGemm2);
+    // router between the plan and the fused kernel (gate_inline): it reads only
+    // x and the router weights, so it neither waits for the plan nor holds the
+    // fused kernel's launch (which waits for this grid — and, transitively,
+    // the plan — at its pdl_wait)
+    if (kMode == 0 && c.gate_inline) pdl_launch_dependents();
     tl_start(c, kTlId);
     int total;
     if (kMode == 0) {
@@ -784,6 +789,22 @@ void launch_gate_tc(const CUtensorMap& tx, const CUtensorMap& twg, const DevCtx&
     const int tiles = (c.S + kBM - 1) / kBM;
     const int ks = c.gate_splits;
     GemmArgs g{1, c.H / kBK / ks, 0, c.E > 128 ? 2 : 1, tiles * ks, ks};
+    if (c.gate_inline && c.pdl) {
+        // behind the permute/plan kernel, launched early (it reads only x and
+        // the router weights; see run_phase)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(std::min(grid, tiles * ks));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = kGemmSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        (void)cudaLaunchKernelEx(&cfg, k_gemm<0>, tx, twg, c, g);
+        return;
+    }
     k_gemm<0><<<std::min(grid, tiles * ks), 256, kGemmSmem, st>>>(tx, twg, c, g);
 }
 

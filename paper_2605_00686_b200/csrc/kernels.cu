@@ -229,30 +229,55 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         return;
     }
     tl_start(c, kTlPerm);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(sm);  // [E][kPermT / 32]
-    int32_t* base = sm + E * (kPermT / 32);             // [E]
+    if (tid == 0) tl_mark(c, kTlPermBlkStart);
+    // Per-expert shared arrays are stored at a swizzled expert slot: with the
+    // balanced routing a warp's lanes hit experts 8 apart, which all fall in one
+    // bank at a stride of 8 words (16-way conflicts); the XOR spreads them over
+    // all 32 banks.  A bijection on [0, E) when E is a multiple of 32.
+    const bool swz = (E & 31) == 0;
+    auto sw = [swz](int e) { return swz ? e ^ ((e >> 3) & 31) : e; };
+    uint32_t* bits = reinterpret_cast<uint32_t*>(sm);  // [kPermT / 32][E] (swizzled expert slot)
+    int32_t* base = sm + E * (kPermT / 32);             // [E] (swizzled)
     int32_t* tot = base + E;                            // [E]
     int32_t* scratch = tot + E;                         // [33]
+    int32_t* pre = scratch + 40;                        // [kPermT / 32][E] (swizzled)
+    int32_t* part = pre + E * (kPermT / 32);            // [kPermT][2] histogram partial sums
     for (int i = tid; i < E * (kPermT / 32); i += kPermT) bits[i] = 0;
     const int32_t* hist = c.hist + size_t(c.par) * c.hist_blocks * E;
     int32_t* hist_next = c.hist + size_t(c.par ^ 1) * c.hist_blocks * E;  // zeroed for the next forward
+    // the block histograms: G = kPermT / E threads per expert (E <= 256), each
+    // summing every G-th block with up to 16 loads in flight (latency-bound)
+    {
+        const int G = kPermT / E;
+        if (tid < G * E) {
+            const int e = tid % E, h = tid / E;
+            int32_t before = 0, after = 0;
+            int q = h;
+            for (; q + 15 * G < nb; q += 16 * G) {
+                int32_t v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = hist[size_t(q + u * G) * E + e];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    if (q + u * G < b) before += v[u]; else after += v[u];
+                }
+            }
+            for (; q < nb; q += G) {
+                const int32_t v = hist[size_t(q) * E + e];
+                if (q < b) before += v; else after += v;
+            }
+            part[2 * tid] = before;
+            part[2 * tid + 1] = after;
+        }
+        __syncthreads();
+    }
     for (int e = tid; e < E; e += kPermT) {
         int32_t before = 0, after = 0;
-        int q = 0;
-        for (; q + 8 <= nb; q += 8) {  // 8 independent loads in flight (latency-bound kernel)
-            int32_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = hist[size_t(q + u) * E + e];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (q + u < b) before += v[u]; else after += v[u];
-            }
+        for (int h = 0; h < kPermT / E; ++h) {
+            before += part[2 * (h * E + e)];
+            after += part[2 * (h * E + e) + 1];
         }
-        for (; q < nb; ++q) {
-            const int32_t v = hist[size_t(q) * E + e];
-            if (q < b) before += v; else after += v;
-        }
-        base[e] = before;
+        base[sw(e)] = before;
         tot[e] = before + after;
         hist_next[size_t(b) * E + e] = 0;
         if (b == 0) {
@@ -262,6 +287,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         }
     }
     __syncthreads();
+    if (tid == 0) tl_mark(c, kTlPermHist);
     if (b == 0 && tid == 0) {
         // one fence (cumulative over the CTA barrier above: every thread's
         // count_table stores), then the per-source ready flag at every PE.  The
@@ -279,10 +305,11 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     }
     const int32_t total = block_exclusive_scan(tot, E, scratch);
     for (int e = tid; e < E; e += kPermT) {
-        base[e] += tot[e];
+        base[sw(e)] += tot[e];
         if (b == 0) c.offsets[e] = tot[e];
     }
     if (b == 0 && tid == 0) c.offsets[E] = total;
+    if (tid == 0) tl_mark(c, kTlPermScan);
     const int t = b * kPermT + tid;
     int32_t my[16];
     if (t < c.S) {
@@ -291,21 +318,45 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
             if (j < c.k) my[j] = c.ids[size_t(t) * c.k + j];
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-            if (j < c.k) atomicOr(&bits[my[j] * (kPermT / 32) + (tid >> 5)], 1u << (tid & 31));
+            if (j < c.k) atomicOr(&bits[(tid >> 5) * E + sw(my[j])], 1u << (tid & 31));
     }
     __syncthreads();
+    // per expert, the tokens of the earlier warps of this block (one pass, so a
+    // token's rank is two shared loads instead of a popcount over every earlier warp)
+    for (int e = tid; e < E; e += kPermT) {
+        int32_t acc = 0;
+#pragma unroll
+        for (int q = 0; q < kPermT / 32; ++q) {
+            pre[q * E + sw(e)] = acc;
+            acc += __popc(bits[q * E + sw(e)]);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) tl_mark(c, kTlPermBits);
     const int w = tid >> 5;
     const uint32_t below = (1u << (tid & 31)) - 1u;
-    // token dedup: this token's row in each remote destination's token buffer
-    // (tokens in ascending order per destination: earlier blocks, earlier warps,
-    // earlier lanes)
-    __shared__ int32_t dwarp[kPermT / 32][kMaxPes], dbase[kMaxPes];
-    int32_t u_of[kMaxPes];
+    if (t < c.S) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j >= c.k) break;
+            const int se = sw(my[j]), i = w * E + se;
+            const int32_t p = base[se] + pre[i] + __popc(bits[i] & below);
+            c.rows[p] = t;
+            c.pos[size_t(t) * c.k + j] = p;
+        }
+    }
     if (c.dedup) {
+        // token dedup: this token's row in each remote destination's token buffer
+        // (tokens in ascending order per destination: earlier blocks, earlier
+        // warps, earlier lanes), stored per (expert, row) slot
+        __shared__ int32_t dwarp[kPermT / 32][kMaxPes], dbase[kMaxPes];
+        int32_t u_of[kMaxPes];
         unsigned dm = 0;
-        if (t < c.S)
-            for (int j = 0; j < c.k; ++j)
-                if (my[j] % c.P != c.rank) dm |= 1u << (my[j] % c.P);
+        if (t < c.S) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < c.k && my[j] % c.P != c.rank) dm |= 1u << (my[j] % c.P);
+        }
 #pragma unroll
         for (int d = 0; d < kMaxPes; ++d) {
             const unsigned bal = __ballot_sync(0xffffffffu, d < c.P && (dm >> d & 1u));
@@ -327,32 +378,25 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         __syncthreads();
 #pragma unroll
         for (int d = 0; d < kMaxPes; ++d) {
-            if (d >= c.P) break;
-            int32_t off = dbase[d];
-            for (int q = 0; q < w; ++q) off += dwarp[q][d];
+            int32_t off = d < c.P ? dbase[d] : 0;
+            for (int q = 0; q < w; ++q) off += d < c.P ? dwarp[q][d] : 0;
             u_of[d] += off;
         }
-    }
-    if (t >= c.S) return;
+        if (t < c.S) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (j >= c.k) break;
-        const uint32_t* row = bits + my[j] * (kPermT / 32);
-        int32_t rank = __popc(row[w] & below);
-        for (int q = 0; q < w; ++q) rank += __popc(row[q]);
-        const int32_t p = base[my[j]] + rank;
-        c.rows[p] = t;
-        c.pos[size_t(t) * c.k + j] = p;
-        if (c.dedup) {
-            const int d = my[j] % c.P;
-            int32_t u = -1;
+            for (int j = 0; j < 16; ++j) {
+                if (j >= c.k) break;
+                const int d = my[j] % c.P;
+                int32_t u = -1;
 #pragma unroll
-            for (int q = 0; q < kMaxPes; ++q)
-                if (q == d && d != c.rank) u = u_of[q];
-            c.uidx[p] = u;
+                for (int q = 0; q < kMaxPes; ++q) u = (q == d && d != c.rank) ? u_of[q] : u;
+                const int se = sw(my[j]), i = w * E + se;
+                c.uidx[base[se] + pre[i] + __popc(bits[i] & below)] = u;
+            }
         }
     }
     tl_end(c, kTlPerm, tid == 0);
+    if (tid == 0) tl_mark(c, kTlPermBlkEnd);
 }
 
 // ------------------------------------------------------------------ plan ----
@@ -570,7 +614,15 @@ void launch_route(const DevCtx& c, bool with_plan, cudaStream_t st) {
 }
 
 size_t perm_smem_bytes(const DevCtx& c) {
-    return sizeof(int32_t) * (size_t(c.E) * (kPermT / 32) + 2 * size_t(c.E) + 40);
+    // At least 32 KB: the router GEMM (211 KB of shared memory per CTA) runs
+    // beside this grid, and a router CTA sharing an SM with the plan CTA
+    // doubled the plan's critical path (measured: plan end 22.1 -> 17.0 us into
+    // the forward with the reservation).  PERSEUS_PERM_SMEM_KB overrides.
+    static const size_t floor_b = [] {
+        const char* e = getenv("PERSEUS_PERM_SMEM_KB");
+        return e ? size_t(atoi(e)) * 1024 : size_t(32) * 1024;
+    }();
+    return std::max(floor_b, sizeof(int32_t) * (2 * size_t(c.E) * (kPermT / 32) + 2 * size_t(c.E) + 40 + 2 * kPermT));
 }
 
 void launch_plan(const DevCtx& c, cudaStream_t st) {

@@ -403,11 +403,21 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
                            size_t(L->Y_rows) * L->H * 2, st), "poison ybuf");
     }
     // Reference routing modes: the expert ids do not depend on the logits, so the
-    // router GEMM runs on a side stream, overlapped with route/permute/plan, and
-    // only the routing weights (written by the fused kernel) wait for it.
-    static const bool side_ok = [] { const char* e = getenv("PERSEUS_SIDE_GATE"); return !e || atoi(e) != 0; }();
-    const bool side_gate = side_ok && all && L->fused && L->cfg.routing != PERSEUS_ROUTE_GATE;
-    c.weights_late = side_gate;
+    // router GEMM runs beside route/permute/plan and only the routing weights
+    // (written by the fused kernel's copy warps) wait for it.  With PDL the
+    // router is launched in the stream AFTER the permute/plan kernel and
+    // triggers its dependents at once: it starts while the plan is built, and
+    // the fused kernel launches early behind it (its pdl_wait covers router and
+    // plan) — no cross-stream event, which would serialise the fused kernel's
+    // launch (measured ~10 us from plan end to fused start with the event).
+    // Without PDL: the router on a side stream, joined by an event before the
+    // fused kernel.  PERSEUS_SIDE_GATE=0 / 1 / 2 forces serial / side stream / inline.
+    static const int side_env = [] { const char* e = getenv("PERSEUS_SIDE_GATE"); return e ? atoi(e) : -1; }();
+    const int side_mode = side_env >= 0 ? side_env : (c.pdl ? 2 : 1);
+    const bool late_ok = all && L->fused && L->cfg.routing != PERSEUS_ROUTE_GATE;
+    const bool side_gate = late_ok && side_mode == 1;
+    c.gate_inline = late_ok && side_mode == 2 ? 1 : 0;
+    c.weights_late = side_gate || c.gate_inline;
     // pair order: at least one wave of GEMM1 items on self pairs before the
     // remote pairs (the lag of launch_moe2's item interleave)
     c.self_head = std::max(1, (L->num_sms / 2 + L->I / 128 - 1) / (L->I / 128));
@@ -425,10 +435,11 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
             ck(cudaStreamWaitEvent(L->stream2, L->ev_x, 0), "wait");
             launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, L->stream2);
             ck(cudaEventRecord(L->ev_gate, L->stream2), "event");
-        } else {
-            launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, st);
+        } else if (!c.gate_inline) {
+            launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, st);  // serial
         }
         launch_route(c, /*with_plan=*/all, st);
+        if (c.gate_inline) launch_gate_tc(L->tm_x, L->tm_wg, c, L->num_sms, st);  // after the plan, early (PDL)
     }
     if (tev) ck(cudaEventRecord(L->ev[1], st), "event");
     if (all && L->fused) {

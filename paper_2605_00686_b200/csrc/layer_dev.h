@@ -37,7 +37,8 @@ struct DevCtx {
     int32_t* hist;       // [2][hist_blocks][E]: per-256-token-block expert histogram (parity halves)
     int32_t hist_blocks; // ceil(S/256)
     int32_t gate_splits; // tensor-core router: K splits, logits = sum of [gate_splits][S][E] partials
-    int32_t weights_late; // 1: the router ran on a side stream; the fused kernel's copy warps write weights
+    int32_t weights_late; // 1: the router ran beside route/permute/plan; the fused kernel's copy warps write weights
+    int32_t gate_inline;  // 1: the router runs in the stream after the plan kernel, launched early (PDL)
     const int32_t* zipf_ids;  // [S*k]: reference Zipf draws (routing == ZIPF)
     bf16* hbuf;          // [R_max][I]
 
@@ -103,7 +104,8 @@ struct DevCtx {
 
 // kernel ids of the diagnostic timeline (DevCtx::tl)
 enum TlKernel : int { kTlGate = 0, kTlRoute, kTlPerm, kTlPlan, kTlFused, kTlCombine, kTlDispatch, kTlGemm1, kTlGemm2,
-                      kTlMmaOut, kTlCopyEnd, kTlEpiEnd, kTlCounts, kTlPlanReady, kTlFusedEnter, kTlPlanB, kTlPlanC, kTlCount };
+                      kTlMmaOut, kTlCopyEnd, kTlEpiEnd, kTlCounts, kTlPlanReady, kTlFusedEnter, kTlPlanB, kTlPlanC,
+                      kTlPermBlkStart, kTlPermBlkEnd, kTlPermHist, kTlPermScan, kTlPermBits, kTlCount };
 
 #ifdef __CUDACC__
 // Launch with programmatic stream serialization (the kernel calls pdl_wait()

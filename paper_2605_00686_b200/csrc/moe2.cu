@@ -716,7 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 else combine_token_warp<16>(c, int(uint32_t(v)), lane);
             }
         } else if (c.weights_late) {
-            // the routing weights (router GEMM ran on a side stream), after the puts
+            // the routing weights (router GEMM ran beside route/permute/plan), after the puts
             const int cw = warp < 4 ? warp - 2 : warp - 6;  // 0..5
             for (int t = blockIdx.x * 6 + cw; t < c.S; t += gridDim.x * 6) route_weights_warp(c, t, lane);
         }
@@ -949,12 +949,21 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the plan kernel
         attr[na++].val.programmaticStreamSerializationAllowed = 1;
     }
-    attr[na].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
-    attr[na++].val.cooperative = 1;
+    // Cooperative launch (all CTAs co-resident before any runs) also keeps the
+    // grid from launching early under PDL (measured: tools/microbench/launch_gap,
+    // +2.5 us per forward), so with PDL it is left off: the grid is one CTA per
+    // SM and nothing before it waits for it, so every CTA becomes resident once
+    // route/permute/plan exit.  Without PDL (ranks sharing a device) it stays.
+    static const int coop_env = [] { const char* e = getenv("PERSEUS_COOP"); return e ? atoi(e) : -1; }();
+    const bool coop = coop_env >= 0 ? coop_env != 0 : !c.pdl;
+    if (coop) {
+        attr[na].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (cross-CTA tile dependencies)
+        attr[na++].val.cooperative = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);
-    if (e != cudaSuccess) {
+    if (e != cudaSuccess && coop) {
         (void)cudaGetLastError();
         cfg.numAttrs = na - 1;  // cooperative + clusters rejected: 1 CTA/SM, grid = #SMs keeps them co-resident
         e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k_moe2), args);

@@ -187,7 +187,8 @@ class MoELayer:
 
     TIMELINE_KERNELS = ("router", "route", "permute", "plan", "fused", "combine", "dispatch", "gemm1", "gemm2",
                         "mma_out_of_work", "copy_warps_done", "epilogue_done", "counts_published", "plan_counts_ready",
-                        "fused_cta_entry", "plan_phase_b", "plan_phase_c")
+                        "fused_cta_entry", "plan_phase_b", "plan_phase_c", "perm_block_start", "perm_block_end",
+                        "perm_hist_read", "perm_scan", "perm_bits")
 
     def info(self) -> dict:
         """The forward path chosen at create: fused kernel, CTA-pair tiles."""
