@@ -32,19 +32,23 @@ def main():
     from tests.gpu_util import assert_close, bf16_bits
 
     orc = Oracle()
+    from paper_2605_00686_b200 import _lib
     cases = [
-        ("balanced", 0.0, pb.combined_protocol(0), 2048, 768, 128, 8, 4096),  # the bench configuration
-        ("balanced", 0.0, pb.combined_protocol(0), 2048, 768, 128, 8, 512),
-        ("balanced", 0.0, pb.vanilla_protocol(), 2048, 768, 128, 8, 512),
-        ("zipf", 1.2, pb.combined_protocol(0), 1024, 512, 16 * world, 4, 768),
-        ("gate", 0.0, pb.decoupled_protocol(0), 512, 256, 8 * world, 2, 1024),
+        ("balanced", 0.0, pb.combined_protocol(0), 2048, 768, 128, 8, 4096, 0),  # the bench configuration
+        ("balanced", 0.0, pb.combined_protocol(0), 2048, 768, 128, 8, 512, 0),
+        ("balanced", 0.0, pb.vanilla_protocol(), 2048, 768, 128, 8, 512, 0),
+        ("zipf", 1.2, pb.combined_protocol(0), 1024, 512, 16 * world, 4, 768, 0),
+        ("gate", 0.0, pb.decoupled_protocol(0), 512, 256, 8 * world, 2, 1024, 0),
+        # token dedup dispatch (PERSEUS_F_DEDUP): same outputs, its own fence accounting
+        ("balanced", 0.0, pb.combined_protocol(0), 2048, 768, 128, 8, 4096, _lib.F_DEDUP),
+        ("zipf", 1.2, pb.combined_protocol(0), 2048, 768, 128, 8, 1024, _lib.F_DEDUP),
     ]
     results = []
     ok = True
-    for routing, skew, proto, H, I, E, k, S in cases:
+    for routing, skew, proto, H, I, E, k, S, lflags in cases:
         m = pb.ModelConfig("m", H, I, E, k)
         layer = pb.MoELayer(m, S, rank=rank, world=world, device=local, routing=routing, skew=skew,
-                            seed=7, protocol=proto, pair=True)  # the CTA-pair kernel even at small S
+                            seed=7, protocol=proto, pair=True, flags=lflags)  # the CTA-pair kernel even at small S
         layer.connect_dist()
         x = torch.empty(S, H, dtype=torch.bfloat16, device="cuda")
         out = torch.empty_like(x)
@@ -53,7 +57,7 @@ def main():
             layer.forward(x, out)
         torch.cuda.synchronize()
         dist.barrier()
-        r = {"routing": routing, "protocol": proto.mode_name(), "rank": rank}
+        r = {"routing": routing, "protocol": proto.mode_name() + ("+dedup" if lflags else ""), "rank": rank}
         try:
             c = layer.counters()
             assert c["wait_timeouts"] == 0 and c["errors"] == 0, c
@@ -66,6 +70,8 @@ def main():
             own = want[want[:, 0] == rank]
             exp = orc.fences_for_src(own, rank, 0 if proto.signaling == "coupled" else 1, proto.group_size)
             per_fwd = c["dispatch_fences"] / 3
+            if lflags:  # dedup: one fence per remote destination this rank sends to
+                exp = len({int(t[1]) for t in own})
             assert per_fwd == exp, (per_fwd, exp)
             shape = LayerShape(H, I, E, k, S, world)
             ids, w, counts, pos = layer.routing()

@@ -8,4 +8,4 @@ python -c "
 import json; d=json.load(open('gpurun_out/r02_mgpu_check_ep4.json'))
 print(d['mgpu_check'], [(r[0]['routing'], r[0]['protocol'], all(x['ok'] for x in r), r[0].get('rel_err')) for r in d['results']])
 [print(t['protocol'], t['violations'], t['conservation'], t['dispatch']['fence_count'], t['dispatch']['flagged_signal_count']) for t in d['device_trace']]"
-TAG=r02f bash tools/mgpu_bench.sh
+TAG=${TAG:-r02f} SKIP_NCCL=${SKIP_NCCL:-} bash tools/mgpu_bench.sh
