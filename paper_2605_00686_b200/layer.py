@@ -60,8 +60,20 @@ class MoELayer:
     def __init__(self, model: ModelConfig, tokens_per_pe: int, rank: int = 0, world: int = 1,
                  device: int = 0, routing: str = "balanced", skew: float = 0.0, seed: int = 1,
                  protocol: Optional[ProtocolConfig] = None, synthetic_weights: bool = True,
-                 fused: bool = True, pair: Optional[bool] = None, pdl: bool = True, flags: int = 0):
+                 fused: bool = True, pair: Optional[bool] = None, pdl: Optional[bool] = None, flags: int = 0):
         protocol = protocol or combined_protocol(0)
+        if pdl is None:
+            # PDL unless several EP ranks (processes) share one device: a grid
+            # waiting for its PDL primary holds up the device's work distributor,
+            # and with it the other ranks' grids that primary waits for
+            import os
+            shared = os.environ.get("PERSEUS_SHARED_DEVICE")
+            if shared is None:
+                import torch
+                n_dev = torch.cuda.device_count()
+                pdl = not (world > 1 and n_dev > 0 and world > n_dev)
+            else:
+                pdl = not int(shared)
         self.fused = fused
         self.model, self.S, self.rank, self.world, self.device = model, tokens_per_pe, rank, world, device
         self.routing_mode, self.skew, self.seed, self.protocol = routing, skew, seed, protocol
