@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         return;
     }
     tl_start(c, kTlPerm);
-    if (tid == 0) tl_mark(c, kTlPermBlkStart);
+    const uint64_t t_blk = tl_now(c);
     // Per-expert shared arrays are stored at a swizzled expert slot: with the
     // balanced routing a warp's lanes hit experts 8 apart, which all fall in one
     // bank at a stride of 8 words (16-way conflicts); the XOR spreads them over
@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         }
     }
     __syncthreads();
-    if (tid == 0) tl_mark(c, kTlPermHist);
+    const uint64_t t_hist = tl_now(c);
+    uint64_t t_counts = 0;
     if (b == 0 && tid == 0) {
         // one fence (cumulative over the CTA barrier above: every thread's
         // count_table stores), then the per-source ready flag at every PE.  The
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         if (c.P > 1) fence_acq_rel_sys();
         else fence_acq_rel_gpu();
         for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
-        tl_mark(c, kTlCounts);
+        t_counts = tl_now(c);
     }
     if (c.dedup && b == 0 && tid < c.P) {  // rows of the reference layout this rank sends to each PE
         int32_t r = 0;
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         if (b == 0) c.offsets[e] = tot[e];
     }
     if (b == 0 && tid == 0) c.offsets[E] = total;
-    if (tid == 0) tl_mark(c, kTlPermScan);
+    const uint64_t t_scan = tl_now(c);
     const int t = b * kPermT + tid;
     int32_t my[16];
     if (t < c.S) {
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         }
     }
     __syncthreads();
-    if (tid == 0) tl_mark(c, kTlPermBits);
+    const uint64_t t_bits = tl_now(c);
     const int w = tid >> 5;
     const uint32_t below = (1u << (tid & 31)) - 1u;
     if (t < c.S) {
@@ -396,7 +397,14 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         }
     }
     tl_end(c, kTlPerm, tid == 0);
-    if (tid == 0) tl_mark(c, kTlPermBlkEnd);
+    if (tid == 0) {
+        tl_at(c, kTlPermBlkStart, t_blk);
+        tl_at(c, kTlPermHist, t_hist);
+        tl_at(c, kTlCounts, t_counts);
+        tl_at(c, kTlPermScan, t_scan);
+        tl_at(c, kTlPermBits, t_bits);
+        tl_mark(c, kTlPermBlkEnd);
+    }
 }
 
 // ------------------------------------------------------------------ plan ----

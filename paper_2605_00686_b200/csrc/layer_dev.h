@@ -149,6 +149,14 @@ __device__ __forceinline__ void tl_mark(const DevCtx& c, int id) {
     atomicMax(c.tl + 2 * id, ~t);
     atomicMax(c.tl + 2 * id + 1, t);
 }
+// ... recorded later (a time taken with tl_now): the atomics stay off the
+// critical path of latency-bound code that synchronises right after the point
+__device__ __forceinline__ uint64_t tl_now(const DevCtx& c) { return c.tl ? fwd_now() : 0; }
+__device__ __forceinline__ void tl_at(const DevCtx& c, int id, uint64_t t) {
+    if (!c.tl || !t) return;
+    atomicMax(c.tl + 2 * id, ~t);
+    atomicMax(c.tl + 2 * id + 1, t);
+}
 
 // Append one event to the device event log (trace mode only).
 __device__ __forceinline__ void trace_ev(const DevCtx& c, int kind, int peer, int tile, int group, uint32_t bytes,

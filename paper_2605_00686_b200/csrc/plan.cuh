@@ -88,7 +88,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         s_err = 1;
     }
     sync128();
-    if (tid == 0) tl_mark(c, kTlPlanReady);
+    const uint64_t t_ready = tl_now(c);
     const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
     #pragma unroll 1
     for (int i = tid; i < PE; i += kPlanThreads) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
@@ -230,7 +230,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         }
     }
     sync128();
-    if (tid == 0) tl_mark(c, kTlPlanB);
+    const uint64_t t_b = tl_now(c);
 
     const int gs = c.group_size;
     const int32_t n_send = s_n_send, n_recv = s_n_recv, n_pairs = s_n_pairs, rows_in_r = s_rows_in;
@@ -383,7 +383,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         }
     }
     sync128();
-    if (tid == 0) tl_mark(c, kTlPlanC);
+    const uint64_t t_c = tl_now(c);
     if (tid == 0) {
         PlanHeader h;
         h.n_send = n_send;
@@ -399,6 +399,9 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
         h.remote_rows_in = rows_in_r;
         *c.hdr = h;
         if (s_err) atomicAdd(&c.stats[kStatErrors], 1ull);
+        tl_at(c, kTlPlanReady, t_ready);
+        tl_at(c, kTlPlanB, t_b);
+        tl_at(c, kTlPlanC, t_c);
     }
 }
 
