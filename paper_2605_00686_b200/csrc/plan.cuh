@@ -350,19 +350,20 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             int n_all = 0;
             #pragma unroll 1
             for (int a = 0; a < P; ++a) n_all += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
-            // recv position of list position li of expert j (arrival order)
-            auto tile_at = [&](int li) {
-                #pragma unroll 1
-                for (int a = 0; a < P; ++a) {
-                    const int s = (r - a + P) % P;
-                    const int nt = ceil_tiles(T[s * E + r + P * j]);
-                    if (li < nt) {
-                        const int ks = s == r ? 0 : (s < r ? s + 1 : s);
-                        return rp[ks * El + j] + li;
-                    }
-                    li -= nt;
+            // recv positions of expert j's tiles in list (arrival) order: a cursor
+            // that only moves forward (pairs take list positions 2m, 2m + 1, ...)
+            int ca = 0, cstart = 0, cnt = ceil_tiles(T[r * E + r + P * j]), cur = 0;
+            int cpos = rp[j];  // recv position of class 0's (self) first tile
+            auto next_tile = [&]() {
+                while (cur - cstart >= cnt) {
+                    cstart += cnt;
+                    ++ca;
+                    const int s = (r - ca + P) % P;
+                    cnt = ceil_tiles(T[s * E + r + P * j]);
+                    const int ks = s == r ? 0 : (s < r ? s + 1 : s);
+                    cpos = rp[ks * El + j];
                 }
-                return -1;
+                return cpos + (cur++ - cstart);
             };
             int a = 0, lim = ceil_tiles(T[r * E + r + P * j]), in_cls = 0;
             #pragma unroll 1
@@ -375,9 +376,11 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                 }
                 const int q = pp[a * El + j] + in_cls++;
                 const int po = a == 0 ? (q < head ? q : q + (n_pairs - n0)) : head + (q - n0);
+                const int t0 = next_tile();
+                const int t1 = 2 * m + 1 < n_all ? next_tile() : -1;
                 if (po < c.max_recv) {
-                    c.pairs[2 * po] = tile_at(2 * m);
-                    c.pairs[2 * po + 1] = 2 * m + 1 < n_all ? tile_at(2 * m + 1) : -1;
+                    c.pairs[2 * po] = t0;
+                    c.pairs[2 * po + 1] = t1;
                 }
             }
         }
