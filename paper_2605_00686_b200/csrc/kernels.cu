@@ -214,7 +214,12 @@ __global__ void __launch_bounds__(kPermT) k_hist(DevCtx c) {
 
 __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33*/);
 
+// K: the top-k (8, or 0 = any k <= 16); DEDUP: the token-dedup buffer rows.
+// Specialised so the common kernel carries no code it does not run — the
+// kernel is instruction-fetch bound (half its stall samples, ncu).
+template <int K, bool DEDUP>
 __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
+    constexpr int KM = K > 0 ? K : 16;
     pdl_wait();
     pdl_launch_dependents();
     extern __shared__ int32_t sm[];
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
         t_counts = tl_now(c);
     }
-    if (c.dedup && b == 0 && tid < c.P) {  // rows of the reference layout this rank sends to each PE
+    if (DEDUP && b == 0 && tid < c.P) {  // rows of the reference layout this rank sends to each PE
         int32_t r = 0;
         for (int e = tid; e < E; e += c.P) r += tot[e];
         c.drows[tid] = r;
@@ -312,14 +317,15 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     if (b == 0 && tid == 0) c.offsets[E] = total;
     const uint64_t t_scan = tl_now(c);
     const int t = b * kPermT + tid;
-    int32_t my[16];
+    const int k = K > 0 ? K : c.k;
+    int32_t my[KM];
     if (t < c.S) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (j < c.k) my[j] = c.ids[size_t(t) * c.k + j];
+        for (int j = 0; j < KM; ++j)
+            if (j < k) my[j] = c.ids[size_t(t) * k + j];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (j < c.k) atomicOr(&bits[(tid >> 5) * E + sw(my[j])], 1u << (tid & 31));
+        for (int j = 0; j < KM; ++j)
+            if (j < k) atomicOr(&bits[(tid >> 5) * E + sw(my[j])], 1u << (tid & 31));
     }
     __syncthreads();
     // per expert, the tokens of the earlier warps of this block (one pass, so a
@@ -338,15 +344,15 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     const uint32_t below = (1u << (tid & 31)) - 1u;
     if (t < c.S) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (j >= c.k) break;
+        for (int j = 0; j < KM; ++j) {
+            if (j >= k) break;
             const int se = sw(my[j]), i = w * E + se;
             const int32_t p = base[se] + pre[i] + __popc(bits[i] & below);
             c.rows[p] = t;
-            c.pos[size_t(t) * c.k + j] = p;
+            c.pos[size_t(t) * k + j] = p;
         }
     }
-    if (c.dedup) {
+    if constexpr (DEDUP) {
         // token dedup: this token's row in each remote destination's token buffer
         // (tokens in ascending order per destination: earlier blocks, earlier
         // warps, earlier lanes), stored per (expert, row) slot
@@ -355,8 +361,8 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         unsigned dm = 0;
         if (t < c.S) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (j < c.k && my[j] % c.P != c.rank) dm |= 1u << (my[j] % c.P);
+            for (int j = 0; j < KM; ++j)
+                if (j < k && my[j] % c.P != c.rank) dm |= 1u << (my[j] % c.P);
         }
 #pragma unroll
         for (int d = 0; d < kMaxPes; ++d) {
@@ -385,8 +391,8 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         }
         if (t < c.S) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (j >= c.k) break;
+            for (int j = 0; j < KM; ++j) {
+                if (j >= k) break;
                 const int d = my[j] % c.P;
                 int32_t u = -1;
 #pragma unroll
@@ -617,8 +623,12 @@ void launch_route(const DevCtx& c, bool with_plan, cudaStream_t st) {
     const int nb = (c.S + kPermT - 1) / kPermT;
     DevCtx cc = c;
     cc.with_plan = with_plan ? 1 : 0;
-    launch_pdl(k_perm, dim3(nb + cc.with_plan), dim3(kPermT), std::max(perm_smem_bytes(c), plan_smem_bytes(c)), st,
-               cc);  // + count publish
+    const dim3 grid(nb + cc.with_plan);
+    const size_t smem = std::max(perm_smem_bytes(c), plan_smem_bytes(c));
+    if (c.k == 8)
+        launch_pdl(c.dedup ? k_perm<8, true> : k_perm<8, false>, grid, dim3(kPermT), smem, st, cc);  // + count publish
+    else
+        launch_pdl(c.dedup ? k_perm<0, true> : k_perm<0, false>, grid, dim3(kPermT), smem, st, cc);
 }
 
 size_t perm_smem_bytes(const DevCtx& c) {
@@ -698,10 +708,14 @@ static cudaError_t combine_carveouts() {
 cudaError_t configure_kernels(const DevCtx& c) {
     cudaError_t e = cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan_smem_bytes(c)));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(std::max(perm_smem_bytes(c), plan_smem_bytes(c))));
-    if (e != cudaSuccess) return e;
-    const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_perm), max_carveout(k_plan4), max_carveout(k_dispatch),
+    for (auto f : {k_perm<8, false>, k_perm<8, true>, k_perm<0, false>, k_perm<0, true>}) {
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(std::max(perm_smem_bytes(c), plan_smem_bytes(c))));
+        if (e != cudaSuccess) return e;
+        e = max_carveout(f);
+        if (e != cudaSuccess) return e;
+    }
+    const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_plan4), max_carveout(k_dispatch),
                               max_carveout(k_gate), max_carveout(k_synth_fill), combine_carveouts<1, false>(),
                               combine_carveouts<2, false>(), combine_carveouts<1, true>(), combine_carveouts<2, true>()};
     for (cudaError_t x : es)

@@ -90,8 +90,24 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     sync128();
     const uint64_t t_ready = tl_now(c);
     const int32_t* table = c.count_table[r] + size_t(c.par) * PE;
-    #pragma unroll 1
-    for (int i = tid; i < PE; i += kPlanThreads) T[i] = int32_t(ld_relaxed_sys(reinterpret_cast<const uint32_t*>(table + i)));
+    {
+        // up to 4 loads in flight per thread (PE <= 4 * kPlanThreads up to P = 8 at E = 128)
+        const uint32_t* tb32 = reinterpret_cast<const uint32_t*>(table);
+        #pragma unroll 1
+        for (int i0 = tid; i0 < PE; i0 += 4 * kPlanThreads) {
+            uint32_t v[4];
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kPlanThreads;
+                v[u] = i < PE ? ld_relaxed_sys(tb32 + i) : 0u;
+            }
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kPlanThreads;
+                if (i < PE) T[i] = int32_t(v[u]);
+            }
+        }
+    }
     if (tid == 0) {
         #pragma unroll 1
         for (int q = 0; q < 8; ++q) c.sched[q] = 0;  // work items, copy queues, dataflow-combine queue
