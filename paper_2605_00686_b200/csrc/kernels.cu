@@ -515,39 +515,84 @@ __global__ void __launch_bounds__(256) k_dispatch(DevCtx c) {
 // sorted slot p is send tile send_first[e] + (p - offsets[e]) / 128.
 template <int K, int CPT, bool CS>
 __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
-    // TPC tokens per CTA, TT = H / (8 * CPT) threads per token, CPT 16-byte
-    // column chunks per thread (all CPT * k loads in flight)
+    // TPC tokens per CTA step, TT = H / (8 * CPT) threads per token, CPT 16-byte
+    // column chunks per thread (all CPT * k loads in flight).  Grid-stride over
+    // token blocks: the launch sizes the grid to the resident CTAs (no partial
+    // last wave) or to one block per CTA.
     pdl_wait();
     tl_start(c, kTlCombine);
     const int TT = c.H / (8 * CPT);
+    const int tpc = blockDim.x / TT;
     const int tl = threadIdx.x / TT, v = threadIdx.x - tl * TT;
-    const int t = blockIdx.x * (blockDim.x / TT) + tl;
     const int k = K > 0 ? K : c.k;
-    const bool live = t < c.S;
-    uint64_t t_start = 0;
-    if (c.P > 1 && threadIdx.x == 0) t_start = fwd_now();
-    if (c.P > 1 && live && v < k && !c.local_combine) {
-        const int e = c.ids[size_t(t) * k + v];
-        if (e % c.P != c.rank) {
-            const int32_t rel = c.pos[size_t(t) * k + v] - c.offsets[e];
-            const int sp = c.send_first[e] + rel / kTileRows;
-            const int tile = c.send[sp].tile_id;
-            if (!wait_flag_geq(c.cflag[c.rank] + size_t(c.par) * c.T_max + tile, c.epoch, kWaitTimeoutNs))
-                atomicAdd(&c.stats[kStatTimeouts], 1ull);
-            if (c.trace && atomicExch(c.trace_seen_ep + tile, c.epoch) != c.epoch) {
-                const SendTile st = c.send[sp];  // the tile's rows came back into our sorted slots
-                trace_seen(c, PERSEUS_EV_COMBINE_SEEN, st.dst, tile,
-                           c.ybuf[c.rank] + (size_t(c.par) * c.Y_rows + c.offsets[e] + st.row0) * c.H, st.rows);
+    const int nblk = (c.S + tpc - 1) / tpc;
+    const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
+    constexpr int KM = K > 0 ? K : 16;
+    unsigned long long waited_max = 0;
+    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int t = blk * tpc + tl;
+        const bool live = t < c.S;
+        uint64_t t_start = 0;
+        if (c.P > 1 && threadIdx.x == 0) t_start = fwd_now();
+        if (c.P > 1 && live && v < k && !c.local_combine) {
+            const int e = c.ids[size_t(t) * k + v];
+            if (e % c.P != c.rank) {
+                const int32_t rel = c.pos[size_t(t) * k + v] - c.offsets[e];
+                const int sp = c.send_first[e] + rel / kTileRows;
+                const int tile = c.send[sp].tile_id;
+                if (!wait_flag_geq(c.cflag[c.rank] + size_t(c.par) * c.T_max + tile, c.epoch, kWaitTimeoutNs))
+                    atomicAdd(&c.stats[kStatTimeouts], 1ull);
+                if (c.trace && atomicExch(c.trace_seen_ep + tile, c.epoch) != c.epoch) {
+                    const SendTile st = c.send[sp];  // the tile's rows came back into our sorted slots
+                    trace_seen(c, PERSEUS_EV_COMBINE_SEEN, st.dst, tile,
+                               c.ybuf[c.rank] + (size_t(c.par) * c.Y_rows + c.offsets[e] + st.row0) * c.H, st.rows);
+                }
             }
         }
+        __syncthreads();
+        if (c.P > 1 && threadIdx.x == 0) waited_max = max(waited_max, (unsigned long long)(fwd_now() - t_start));
+        if (!live) continue;
+        uint4 u[CPT][KM];
+        float w[KM];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            if (j < k) {
+                const int32_t p = c.pos[size_t(t) * k + j];
+                w[j] = c.weights[size_t(t) * k + j];
+#pragma unroll
+                for (int q = 0; q < CPT; ++q)
+                {
+                    const uint4* src = reinterpret_cast<const uint4*>(y + size_t(p) * c.H + (v + q * TT) * 8);
+                    u[q][j] = CS ? __ldcs(src) : *src;  // CS: every y row is read exactly once
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < KM; ++j) {
+                if (j < k) {
+                    const bf16* b = reinterpret_cast<const bf16*>(&u[q][j]);
+#pragma unroll
+                    for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(w[j], __bfloat162float(b[z]), acc[z]);
+                }
+            }
+            uint4 o;
+            o.x = pack_bf16(acc[0], acc[1]);
+            o.y = pack_bf16(acc[2], acc[3]);
+            o.z = pack_bf16(acc[4], acc[5]);
+            o.w = pack_bf16(acc[6], acc[7]);
+            uint4* dst = reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + (v + q * TT) * 8);
+            if (CS) __stcs(dst, o);
+            else *dst = o;
+        }
     }
-    __syncthreads();
     if (c.P > 1 && threadIdx.x == 0) {
         // exposed-communication accounting: the longest any CTA waited for its
         // combine flags; the last CTA folds this forward's timestamps into the stats
-        const unsigned long long waited = fwd_now() - t_start;
-        if (waited > *reinterpret_cast<volatile unsigned long long*>(c.fwd_t + kFwdWaitMax))
-            atomicMax(c.fwd_t + kFwdWaitMax, waited);
+        if (waited_max > *reinterpret_cast<volatile unsigned long long*>(c.fwd_t + kFwdWaitMax))
+            atomicMax(c.fwd_t + kFwdWaitMax, waited_max);
         __threadfence();
         if (atomicAdd(c.fwd_t + kFwdDoneCtas, 1ull) == gridDim.x - 1) {
             __threadfence();
@@ -557,44 +602,6 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
             atomicAdd(&c.stats[kStatCombineSpanNs], span(kFwdCombFirst, kFwdCombLast));
             atomicAdd(&c.stats[kStatCombineWaitNs], ft[kFwdWaitMax]);
         }
-    }
-    if (!live) return;
-    const bf16* y = c.ybuf[c.rank] + size_t(c.par) * c.Y_rows * c.H;
-    constexpr int KM = K > 0 ? K : 16;
-    uint4 u[CPT][KM];
-    float w[KM];
-#pragma unroll
-    for (int j = 0; j < KM; ++j) {
-        if (j < k) {
-            const int32_t p = c.pos[size_t(t) * k + j];
-            w[j] = c.weights[size_t(t) * k + j];
-#pragma unroll
-            for (int q = 0; q < CPT; ++q)
-            {
-                const uint4* src = reinterpret_cast<const uint4*>(y + size_t(p) * c.H + (v + q * TT) * 8);
-                u[q][j] = CS ? __ldcs(src) : *src;  // CS: every y row is read exactly once
-            }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int j = 0; j < KM; ++j) {
-            if (j < k) {
-                const bf16* b = reinterpret_cast<const bf16*>(&u[q][j]);
-#pragma unroll
-                for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(w[j], __bfloat162float(b[z]), acc[z]);
-            }
-        }
-        uint4 o;
-        o.x = pack_bf16(acc[0], acc[1]);
-        o.y = pack_bf16(acc[2], acc[3]);
-        o.z = pack_bf16(acc[4], acc[5]);
-        o.w = pack_bf16(acc[6], acc[7]);
-        uint4* dst = reinterpret_cast<uint4*>(c.out + size_t(t) * c.H + (v + q * TT) * 8);
-        if (CS) __stcs(dst, o);
-        else *dst = o;
     }
     tl_end(c, kTlCombine, threadIdx.x == 0);
 }
@@ -657,17 +664,45 @@ static int combine_cpt(const DevCtx& c) {
     return (c.H % (8 * cpt) == 0 && c.H / (8 * cpt) <= 1024) ? cpt : 1;
 }
 
+// Grid of the combine: one token block per CTA (default), or with
+// PERSEUS_COMBINE_PERSIST=1 the CTAs that fit at once on the device (occupancy x
+// SMs, grid-stride over the token blocks, no partial last wave).  Measured at
+// EP=1 (same box, alternating): K-step 351.6 vs 353.0 us, ncu 30.1 vs 30.7 us —
+// no gain, so the plain grid stays.
+template <typename Kern>
+static dim3 combine_grid(Kern kern, int nblk, int block, int num_sms) {
+    static const bool persist = [] { const char* e = getenv("PERSEUS_COMBINE_PERSIST"); return e && atoi(e) != 0; }();
+    if (!persist) return dim3(nblk);
+    // resident CTAs per SM of this kernel at this block size (cached per thread)
+    thread_local const void* last_k = nullptr;
+    thread_local int last_block = 0, last_per_sm = 0;
+    if (last_k != reinterpret_cast<const void*>(kern) || last_block != block) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, 0) != cudaSuccess) {
+            (void)cudaGetLastError();
+            per_sm = 0;
+        }
+        last_k = reinterpret_cast<const void*>(kern);
+        last_block = block;
+        last_per_sm = per_sm;
+    }
+    if (last_per_sm < 1) return dim3(nblk);
+    return dim3(std::min(nblk, last_per_sm * num_sms));
+}
+
 template <int CPT, bool CS>
-static void launch_combine_cpt(const DevCtx& c, cudaStream_t st) {
+static void launch_combine_cpt(const DevCtx& c, int num_sms, cudaStream_t st) {
     const int tt = c.H / (8 * CPT);                 // threads per token
     const int tpc = std::max(1, 256 / tt);          // tokens per CTA
-    const dim3 grid((c.S + tpc - 1) / tpc), block(tt * tpc);
+    const int nblk = (c.S + tpc - 1) / tpc;
+    const dim3 block(tt * tpc);
+    auto go = [&](auto kern) { launch_pdl(kern, combine_grid(kern, nblk, int(block.x), num_sms), block, 0, st, c); };
     switch (c.k) {
-        case 1: launch_pdl(k_combine<1, CPT, CS>, grid, block, 0, st, c); break;
-        case 2: launch_pdl(k_combine<2, CPT, CS>, grid, block, 0, st, c); break;
-        case 4: launch_pdl(k_combine<4, CPT, CS>, grid, block, 0, st, c); break;
-        case 8: launch_pdl(k_combine<8, CPT, CS>, grid, block, 0, st, c); break;
-        default: launch_pdl(k_combine<0, CPT, CS>, grid, block, 0, st, c); break;
+        case 1: go(k_combine<1, CPT, CS>); break;
+        case 2: go(k_combine<2, CPT, CS>); break;
+        case 4: go(k_combine<4, CPT, CS>); break;
+        case 8: go(k_combine<8, CPT, CS>); break;
+        default: go(k_combine<0, CPT, CS>); break;
     }
 }
 
@@ -680,10 +715,10 @@ static bool combine_cs() {
     return cs;
 }
 
-void launch_combine(const DevCtx& c, cudaStream_t st) {
+void launch_combine(const DevCtx& c, int num_sms, cudaStream_t st) {
     const bool cs = combine_cs();
-    if (combine_cpt(c) == 2) cs ? launch_combine_cpt<2, true>(c, st) : launch_combine_cpt<2, false>(c, st);
-    else cs ? launch_combine_cpt<1, true>(c, st) : launch_combine_cpt<1, false>(c, st);
+    if (combine_cpt(c) == 2) cs ? launch_combine_cpt<2, true>(c, num_sms, st) : launch_combine_cpt<2, false>(c, num_sms, st);
+    else cs ? launch_combine_cpt<1, true>(c, num_sms, st) : launch_combine_cpt<1, false>(c, num_sms, st);
 }
 
 // Every kernel of the forward asks for the maximum shared-memory carveout, so

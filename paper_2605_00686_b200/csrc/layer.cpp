@@ -36,7 +36,7 @@ cudaError_t launch_moe2(const CUtensorMap& a1, const CUtensorMap& b1, const CUte
                         const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
 cudaError_t launch_moe(const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& a2, const CUtensorMap& b2,
                        const DevCtx& c, int64_t a1_row_base, int grid, cudaStream_t st);
-void launch_combine(const DevCtx& c, cudaStream_t st);
+void launch_combine(const DevCtx& c, int num_sms, cudaStream_t st);
 cudaError_t configure_kernels(const DevCtx& c);
 size_t gemm_smem_bytes();
 cudaError_t configure_gemm();
@@ -456,7 +456,7 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
                "launch k_moe");
         if (tev) ck(cudaEventRecord(L->ev[3], st), "event");
         if (tev) ck(cudaEventRecord(L->ev[4], st), "event");
-        if (!c.df_combine) launch_combine(c, st);  // else the fused kernel combined every token
+        if (!c.df_combine) launch_combine(c, L->num_sms, st);  // else the fused kernel combined every token
         if (tev) ck(cudaEventRecord(L->ev[5], st), "event");
         ck(cudaGetLastError(), "kernel launch");
         return;
@@ -470,7 +470,7 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
         launch_gemm(2, L->tm_a2, L->tm_b2, c, L->H / 256, L->I / 64, 0, L->num_sms, st);
     }
     if (tev) ck(cudaEventRecord(L->ev[4], st), "event");
-    if (all || phase == PERSEUS_PHASE_COMBINE) launch_combine(c, st);
+    if (all || phase == PERSEUS_PHASE_COMBINE) launch_combine(c, L->num_sms, st);
     if (tev) ck(cudaEventRecord(L->ev[5], st), "event");
     ck(cudaGetLastError(), "kernel launch");
 }
