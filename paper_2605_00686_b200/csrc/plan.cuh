@@ -34,9 +34,20 @@ __device__ __noinline__ int32_t warp_scan(int32_t* a, int n) {
     __syncwarp();
     const int lane = threadIdx.x & 31;
     const int per = (n + 31) / 32, b = lane * per, e = min(n, b + per);
+    // 16-byte chunks when every lane's run is whole and aligned (n % 128 == 0):
+    // the run's loads are independent instead of one dependent chain
+    const bool vec = (n & 127) == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0;
     int32_t local = 0;
-    #pragma unroll 1
-    for (int i = b; i < e; ++i) local += a[i];
+    if (vec) {
+        #pragma unroll 4
+        for (int i = b; i < e; i += 4) {
+            const int4 q = *reinterpret_cast<const int4*>(a + i);
+            local += (q.x + q.y) + (q.z + q.w);
+        }
+    } else {
+        #pragma unroll 1
+        for (int i = b; i < e; ++i) local += a[i];
+    }
     int32_t incl = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -44,11 +55,22 @@ __device__ __noinline__ int32_t warp_scan(int32_t* a, int n) {
         if (lane >= o) incl += u;
     }
     int32_t run = incl - local;
-    #pragma unroll 1
-    for (int i = b; i < e; ++i) {
-        const int32_t v = a[i];
-        a[i] = run;
-        run += v;
+    if (vec) {
+        #pragma unroll 4
+        for (int i = b; i < e; i += 4) {
+            int4 q = *reinterpret_cast<int4*>(a + i);
+            const int32_t s0 = run, s1 = s0 + q.x, s2 = s1 + q.y, s3 = s2 + q.z;
+            run = s3 + q.w;
+            q = make_int4(s0, s1, s2, s3);
+            *reinterpret_cast<int4*>(a + i) = q;
+        }
+    } else {
+        #pragma unroll 1
+        for (int i = b; i < e; ++i) {
+            const int32_t v = a[i];
+            a[i] = run;
+            run += v;
+        }
     }
     const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
     __syncwarp();
