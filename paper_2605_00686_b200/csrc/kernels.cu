@@ -141,13 +141,8 @@ __device__ __forceinline__ int topk_warp(const float* l, int E, int k, int lane)
 //   GATE     : top-k by descending logit, ties to the lower index (orc_topk)
 //   BALANCED : id[t*k+j] = (t*k+j) mod E (exact capacity, workload.cpp:180-195)
 //   ZIPF     : the reference's Zipf draws (workload.cpp:57-97), host-expanded
-__global__ void __launch_bounds__(256) k_route(DevCtx c) {
-    pdl_wait();
-    pdl_launch_dependents();
-    tl_start(c, kTlRoute);
-    const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (t >= c.S) return;
+// One token of k_route (one warp).
+__device__ __forceinline__ void route_token(const DevCtx& c, int t, int lane) {
     const float* l = c.logits + size_t(t) * c.E;
     int my_id = -1;  // lane j < k holds the j-th chosen expert
     if (c.routing == PERSEUS_ROUTE_GATE) {
@@ -190,6 +185,68 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
         __syncwarp();
         route_weights_warp(c, t, lane);
     }
+}
+
+// Count exchange, by the last CTA of k_route to finish its histogram atomics:
+// this rank's per-expert counts (the block histograms summed) into its row of
+// every PE's [P][E] count table, one fence, then the per-source ready flag at
+// every PE.  Published here rather than by the permutation kernel so the plans
+// (this rank's and the peers') get the counts a kernel launch earlier.
+__device__ __forceinline__ void publish_counts(const DevCtx& c) {
+    __shared__ int s_last;
+    __shared__ int32_t part[256];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this CTA's histogram atomics before its arrival
+        s_last = atomicAdd(c.route_ctr, 1u) == gridDim.x - 1;
+        if (s_last) *c.route_ctr = 0;  // every CTA of this launch has arrived
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int E = c.E, tid = threadIdx.x, nb = c.hist_blocks;
+    const int32_t* hist = c.hist + size_t(c.par) * c.hist_blocks * E;
+    const int G = max(1, int(blockDim.x) / E);  // threads per expert (E <= 256)
+    if (tid < G * E) {
+        const int e = tid % E, h = tid / E;
+        int32_t sum = 0;
+        int q = h;
+        for (; q + 7 * G < nb; q += 8 * G) {
+            int32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(hist + size_t(q + u * G) * E + e);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        for (; q < nb; q += G) sum += __ldcg(hist + size_t(q) * E + e);
+        part[tid] = sum;
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += blockDim.x) {
+        int32_t cnt = 0;
+        for (int h = 0; h < G; ++h) cnt += part[h * E + e];
+        c.counts[e] = cnt;
+        for (int p = 0; p < c.P; ++p) c.count_table[p][(size_t(c.par) * c.P + c.rank) * E + e] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // one fence (cumulative over the CTA barrier: every thread's table
+        // stores), then the flags; the plans acquire them
+        if (c.P > 1) fence_acq_rel_sys();
+        else fence_acq_rel_gpu();
+        for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
+        tl_mark(c, kTlCounts);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_route(DevCtx c) {
+    pdl_wait();
+    pdl_launch_dependents();
+    tl_start(c, kTlRoute);
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t < c.S) route_token(c, t, lane);
+    publish_counts(c);
     tl_end(c, kTlRoute, threadIdx.x == 0);
 }
 
@@ -220,8 +277,12 @@ __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33
 template <int K, bool DEDUP>
 __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     constexpr int KM = K > 0 ? K : 16;
-    pdl_wait();
+    // Trigger before waiting: the next kernel (the router GEMM, which reads only
+    // x and the router weights) may then run beside k_route as well.  Every CTA
+    // of this grid is resident once all have triggered, so nothing behind it can
+    // take their SMs.
     pdl_launch_dependents();
+    pdl_wait();
     extern __shared__ int32_t sm[];
     const int E = c.E, b = blockIdx.x, nb = int(gridDim.x) - c.with_plan, tid = threadIdx.x;
     if (b == nb) {
@@ -285,25 +346,9 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
         base[sw(e)] = before;
         tot[e] = before + after;
         hist_next[size_t(b) * E + e] = 0;
-        if (b == 0) {
-            c.counts[e] = before + after;
-            // count exchange: this rank's row of every PE's [P][E] table
-            for (int p = 0; p < c.P; ++p) c.count_table[p][(size_t(c.par) * c.P + c.rank) * E + e] = before + after;
-        }
     }
     __syncthreads();
-    const uint64_t t_hist = tl_now(c);
-    uint64_t t_counts = 0;
-    if (b == 0 && tid == 0) {
-        // one fence (cumulative over the CTA barrier above: every thread's
-        // count_table stores), then the per-source ready flag at every PE.  The
-        // plan CTA of this same grid acquires the flag, so even P == 1 needs the
-        // release (gpu scope suffices when no peer reads the table).
-        if (c.P > 1) fence_acq_rel_sys();
-        else fence_acq_rel_gpu();
-        for (int p = 0; p < c.P; ++p) st_relaxed_sys(c.count_flag[p] + c.rank, c.epoch);
-        t_counts = tl_now(c);
-    }
+    const uint64_t t_hist = tl_now(c);  // (the counts were published by k_route's last CTA)
     if (DEDUP && b == 0 && tid < c.P) {  // rows of the reference layout this rank sends to each PE
         int32_t r = 0;
         for (int e = tid; e < E; e += c.P) r += tot[e];
@@ -406,7 +451,6 @@ __global__ void __launch_bounds__(kPermT) k_perm(DevCtx c) {
     if (tid == 0) {
         tl_at(c, kTlPermBlkStart, t_blk);
         tl_at(c, kTlPermHist, t_hist);
-        tl_at(c, kTlCounts, t_counts);
         tl_at(c, kTlPermScan, t_scan);
         tl_at(c, kTlPermBits, t_bits);
         tl_mark(c, kTlPermBlkEnd);

@@ -153,6 +153,7 @@ struct perseus_layer {
     bool dedup = false;
     int32_t *dhist = nullptr, *uidx = nullptr, *dtot = nullptr, *drows = nullptr;
     uint32_t *dsent = nullptr, *ex_done = nullptr;
+    uint32_t* route_ctr = nullptr;  // k_route CTAs done (reset by the last)
     uint8_t* peer[kMaxPes] = {};
     bool ipc_mapped[kMaxPes] = {};
     bool connected = false;
@@ -199,6 +200,7 @@ struct perseus_layer {
             }
         }
         c.dedup = dedup ? 1 : 0;
+        c.route_ctr = route_ctr;
         c.dhist = dhist; c.uidx = uidx; c.dtot = dtot; c.drows = drows; c.dsent = dsent; c.ex_done = ex_done;
         c.local_dispatch = (cfg.flags & PERSEUS_F_LOCAL_DISPATCH) ? 1 : 0;
         c.local_combine = (cfg.flags & PERSEUS_F_LOCAL_COMBINE) ? 1 : 0;
@@ -328,7 +330,7 @@ void free_layer(perseus_layer* L) {
                     L->cgroups, L->recv, L->group_ctr, L->cgroup_ctr, L->tile_ctr, L->stats, L->sym,
                     L->sorder, L->rorder, L->send_done, L->g1_done, L->self_ready, L->sched, L->fwd_t, L->tl, L->smaps, L->trace, L->trace_n, L->trace_seen_ep,
                     L->send_first, L->pairs, L->tok_ready, L->ready_q,
-                    L->dhist, L->uidx, L->dtot, L->drows, L->dsent, L->ex_done};
+                    L->dhist, L->uidx, L->dtot, L->drows, L->dsent, L->ex_done, L->route_ctr};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : L->ev)
@@ -540,7 +542,12 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
             L->w2 = dalloc<bf16>(El * H * I);
             L->hbuf = dalloc<bf16>(size_t(L->R_max) * I);
             L->hist_blocks = int((S + 255) / 256);
-            L->gate_splits = (H / 64) % 4 == 0 ? 4 : 1;
+            {
+                // router split-K (partial logits summed by the weights' readers); PERSEUS_GATE_SPLITS overrides
+                static const int gs_env = [] { const char* e = getenv("PERSEUS_GATE_SPLITS"); return e ? atoi(e) : 0; }();
+                const int want = gs_env > 0 ? gs_env : 4;
+                L->gate_splits = (H / 64) % want == 0 ? want : 1;
+            }
             L->logits = dalloc<float>(size_t(L->gate_splits) * S * E);
             L->weights = dalloc<float>(Sk);
             L->ids = dalloc<int32_t>(Sk);
@@ -576,6 +583,7 @@ int perseus_layer_create(const perseus_layer_config* cfg, int rank, int world, i
                 L->dsent = dalloc<uint32_t>(kMaxPes);
                 L->ex_done = dalloc<uint32_t>(L->max_recv);
             }
+            L->route_ctr = dalloc<uint32_t>(1);
             L->tok_ready = dalloc<int32_t>(S);
             L->ready_q = dalloc<unsigned long long>(S);
 

@@ -45,6 +45,7 @@ struct DevCtx {
     // symmetric buffers, one base pointer per PE (peer-mapped; [rank] = local)
     int32_t* count_table[kMaxPes];  // [2][P][E]
     uint32_t* count_flag[kMaxPes];  // [P]
+    uint32_t* route_ctr;            // CTAs of k_route done (the last one publishes the counts)
     bf16* heap[kMaxPes];            // [2][R_max][H]
     uint32_t* dflag[kMaxPes];       // [2][T_max]
     bf16* ybuf[kMaxPes];            // [2][Y_rows][H]
