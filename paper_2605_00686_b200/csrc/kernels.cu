@@ -252,22 +252,12 @@ __global__ void __launch_bounds__(256) k_route(DevCtx c) {
 
 // ----------------------------------------------------------- permutation ----
 // Stable counting sort of the (token, j) pairs by expert (orc_permute): tokens
-// ascending inside each expert segment.  Two passes over 256-token blocks:
-//   k_hist : per-block expert histogram           hist[b][e]
-//   k_perm : segment offsets (scan), then stable in-block ranks from a
-//            per-expert token bitmask (popcount of the lower lanes).
+// ascending inside each expert segment, over 256-token blocks:
+//   k_route: per-block expert histogram hist[b][e] (global atomics)
+//   k_perm : segment offsets (scan of the block histograms), then stable
+//            in-block ranks from a per-expert token bitmask (popcount of the
+//            lower lanes).
 constexpr int kPermT = 256;
-
-__global__ void __launch_bounds__(kPermT) k_hist(DevCtx c) {
-    extern __shared__ int32_t hist[];
-    for (int e = threadIdx.x; e < c.E; e += blockDim.x) hist[e] = 0;
-    __syncthreads();
-    const int t = blockIdx.x * kPermT + threadIdx.x;
-    if (t < c.S)
-        for (int j = 0; j < c.k; ++j) atomicAdd(&hist[c.ids[size_t(t) * c.k + j]], 1);
-    __syncthreads();
-    for (int e = threadIdx.x; e < c.E; e += blockDim.x) c.hist[size_t(blockIdx.x) * c.E + e] = hist[e];
-}
 
 __device__ int32_t block_exclusive_scan(int32_t* a, int n, int32_t* scratch /*33*/);
 
