@@ -49,39 +49,61 @@ void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, flo
 // ------------------------------------------------------------------ gate ----
 // logits[t][e] = sum_h x[t][h] * wg[e][h]: ONE fmaf per h, h ascending — the
 // contract oracle.c:orc_gate_logits restates, so logits (and learned top-k ids)
-// are bit-exact.  CTA tile: 64 tokens x 64 experts; thread: 8 tokens x 2 experts.
-constexpr int kGateT = 64, kGateE = 64, kGateH = 32;
+// are bit-exact.  CTA tile: 64 tokens x 64 experts; thread: 8 tokens x 2 experts
+// (16 independent chains).  128-deep h steps staged through shared memory (fp32,
+// h-major), the next step's tiles loaded into registers while the current one
+// is consumed, so the global load latency hides under 2048 FMAs per thread.
+constexpr int kGateT = 64, kGateE = 64, kGateH = 128;
+constexpr size_t kGateSmem = sizeof(float) * kGateH * (kGateT + kGateE);
 
 __global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const bf16* __restrict__ wg,
                                               float* __restrict__ logits, int S, int H, int E) {
-    __shared__ __align__(16) float xs[kGateH][kGateT];
-    __shared__ __align__(16) float ws[kGateH][kGateE];
+    extern __shared__ __align__(16) float gsm[];
+    float* xs = gsm;                      // [kGateH][kGateT]
+    float* ws = gsm + kGateH * kGateT;    // [kGateH][kGateE]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t0 = blockIdx.x * kGateT, e0 = blockIdx.y * kGateE;
     float acc[8][2];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.f;
 
-    const int lr = tid >> 2, lh = (tid & 3) * 8;  // loader: row, 8-wide h chunk
-    for (int h0 = 0; h0 < H; h0 += kGateH) {
-        {
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (t0 + lr < S) v = *reinterpret_cast<const uint4*>(x + size_t(t0 + lr) * H + h0 + lh);
-            const bf16* b = reinterpret_cast<const bf16*>(&v);
+    // loader: row tid % 64 (a warp = 32 consecutive rows: conflict-free h-major
+    // stores), 8-wide h chunks (tid / 64) + 4 i of the 16 in a step
+    const int lr = tid & 63, lc = tid >> 6;
+    const bool xr = t0 + lr < S, wr = e0 + lr < E;
+    uint4 px[4], pw[4];
+    auto fetch = [&](int h0) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) xs[lh + q][lr] = __bfloat162float(b[q]);
-            uint4 w = make_uint4(0, 0, 0, 0);
-            if (e0 + lr < E) w = *reinterpret_cast<const uint4*>(wg + size_t(e0 + lr) * H + h0 + lh);
-            const bf16* c = reinterpret_cast<const bf16*>(&w);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) ws[lh + q][lr] = __bfloat162float(c[q]);
+        for (int i = 0; i < 4; ++i) {
+            const int h = h0 + (lc + 4 * i) * 8;
+            px[i] = xr && h < H ? *reinterpret_cast<const uint4*>(x + size_t(t0 + lr) * H + h) : make_uint4(0, 0, 0, 0);
+            pw[i] = wr && h < H ? *reinterpret_cast<const uint4*>(wg + size_t(e0 + lr) * H + h) : make_uint4(0, 0, 0, 0);
         }
+    };
+    auto stage = [&]() {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int hh = (lc + 4 * i) * 8;
+            const bf16* b = reinterpret_cast<const bf16*>(&px[i]);
+            const bf16* c = reinterpret_cast<const bf16*>(&pw[i]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                xs[(hh + q) * kGateT + lr] = __bfloat162float(b[q]);
+                ws[(hh + q) * kGateE + lr] = __bfloat162float(c[q]);
+            }
+        }
+    };
+    fetch(0);
+    for (int h0 = 0; h0 < H; h0 += kGateH) {
+        stage();
         __syncthreads();
+        if (h0 + kGateH < H) fetch(h0 + kGateH);  // in flight under this step's FMAs
+        const int hn = min(kGateH, H - h0);
 #pragma unroll 8
-        for (int h = 0; h < kGateH; ++h) {
-            const float4 xa = *reinterpret_cast<const float4*>(&xs[h][warp * 8]);
-            const float4 xb = *reinterpret_cast<const float4*>(&xs[h][warp * 8 + 4]);
-            const float2 wv = *reinterpret_cast<const float2*>(&ws[h][lane * 2]);
+        for (int h = 0; h < hn; ++h) {
+            const float4 xa = *reinterpret_cast<const float4*>(&xs[h * kGateT + warp * 8]);
+            const float4 xb = *reinterpret_cast<const float4*>(&xs[h * kGateT + warp * 8 + 4]);
+            const float2 wv = *reinterpret_cast<const float2*>(&ws[h * kGateE + lane * 2]);
             const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -644,7 +666,7 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
 // bit-exact CUDA-core gate (learned-gate routing)
 void launch_gate_exact(const DevCtx& c, cudaStream_t st) {
     dim3 g((c.S + kGateT - 1) / kGateT, (c.E + kGateE - 1) / kGateE);
-    k_gate<<<g, 256, 0, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
+    k_gate<<<g, 256, kGateSmem, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
 }
 
 // the per-forward plan (plan.cuh), one CTA of 8 warps
@@ -776,6 +798,8 @@ static cudaError_t combine_carveouts() {
 
 cudaError_t configure_kernels(const DevCtx& c) {
     cudaError_t e = cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan_smem_bytes(c)));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGateSmem));
     if (e != cudaSuccess) return e;
     for (auto f : {k_perm<8, false>, k_perm<8, true>, k_perm<0, false>, k_perm<0, true>}) {
         e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
