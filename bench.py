@@ -692,6 +692,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "latency_us": ms_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
+            "timing_note": (f"value = the K = {args.steps} step region, timed on the device with CUDA events; "
+                            "these boxes run power-capped (sw_power_cap), so a long region settles at "
+                            "lower SM clocks than a short burst (round 1 quoted K = 20: ~0.36 ms/step); "
+                            "timing_blocks repeats blocks of the same forward (median / min) and clocks "
+                            "records the SM clock sampled inside"),
             "config": arm_config(args, world, E, proto.mode_name()),
             "stage_ms": dict(zip(["route_permute", "plan_dispatch", "gemm1_swiglu", "gemm2_combine_put",
                                   "combine"] if args.unfused else
