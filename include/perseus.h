@@ -209,8 +209,9 @@ int perseus_layer_forward_host(perseus_layer* layer, const void* x_host, void* o
 /* Pipelined end-to-end forward for a stream of batches (serving): enqueues the
  * H2D copy of x_host on an upload stream, the forward on the layer's stream and
  * the D2H copy into out_host on a download stream, and returns without waiting,
- * so batch n+1's upload and batch n-1's download overlap batch n's forward (two
- * device staging slots).  Host buffers should be pinned and must stay valid
+ * so batch n+1's upload and batch n-1's download overlap batch n's forward
+ * (three device staging slots, so an upload has two forwards' time to land;
+ * PERSEUS_HOST_SLOTS=2 for two).  Host buffers should be pinned and must stay valid
  * until perseus_layer_host_wait(). */
 int perseus_layer_forward_host_async(perseus_layer* layer, const void* x_host, void* out_host);
 /* Wait until every enqueued forward_host_async has its output in host memory. */

@@ -115,9 +115,11 @@ struct perseus_layer {
     bf16 *x_stage = nullptr, *out_stage = nullptr;
     // pipelined host API (perseus_layer_forward_host_async): 2 staging slots,
     // upload / download streams and per-slot events
-    bf16 *xs2[2] = {nullptr, nullptr}, *os2[2] = {nullptr, nullptr};
+    static constexpr int kHostSlots = 3;  // pipelined host batches in flight (forward_host_async)
+    bf16 *xs2[kHostSlots] = {}, *os2[kHostSlots] = {};
     cudaStream_t up = nullptr, down = nullptr;
-    cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_fwd[2] = {nullptr, nullptr}, ev_down[2] = {nullptr, nullptr};
+    cudaEvent_t ev_up[kHostSlots] = {}, ev_fwd[kHostSlots] = {}, ev_down[kHostSlots] = {};
+    int host_slots = 2;  // in use (PERSEUS_HOST_SLOTS, 2..kHostSlots)
     uint64_t host_calls = 0;
     bf16 *wg = nullptr, *w1 = nullptr, *w2 = nullptr, *hbuf = nullptr;
     float *logits = nullptr, *weights = nullptr;
@@ -161,8 +163,10 @@ struct perseus_layer {
     CUtensorMap tm_a1{}, tm_b1{}, tm_a2{}, tm_b2{}, tm_wg{}, tm_x{}, tm_xg{};
     CUtensorMap* smaps = nullptr;  // device copy of the epilogue's TMA store maps (store_maps())
     const void* tm_x_ptr = nullptr;
-    CUtensorMap tm_x_c[2]{}, tm_xg_c[2]{};  // second-level cache: the two pipelined staging slots
-    const void* tm_x_cptr[2] = {nullptr, nullptr};
+    static constexpr int kTmCache = 4;  // second-level cache: the pipelined staging slots (+ the caller's x)
+    CUtensorMap tm_x_c[kTmCache]{}, tm_xg_c[kTmCache]{};
+    const void* tm_x_cptr[kTmCache] = {};
+    int tm_x_next = 0;  // round-robin replacement
     cudaEvent_t ev[6] = {};
     const void* last_x = nullptr;
 
@@ -337,7 +341,7 @@ void free_layer(perseus_layer* L) {
         if (e) cudaEventDestroy(e);
     if (L->stream) cudaStreamDestroy(L->stream);
     if (L->stream2) cudaStreamDestroy(L->stream2);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < perseus_layer::kHostSlots; ++i) {
         if (L->xs2[i]) cudaFree(L->xs2[i]);
         if (L->os2[i]) cudaFree(L->os2[i]);
         for (cudaEvent_t e : {L->ev_up[i], L->ev_fwd[i], L->ev_down[i]})
@@ -376,10 +380,11 @@ void run_phase(perseus_layer* L, int phase, const void* x, void* out, cudaStream
     DevCtx c = L->ctx(x ? x : L->last_x, out);
     if (c.x != L->tm_x_ptr) {  // TMA maps over the caller's token buffer (router tiles + row gathers)
         int hit = -1;
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < perseus_layer::kTmCache; ++i)
             if (L->tm_x_cptr[i] == c.x) hit = i;
         if (hit < 0) {
-            hit = (L->tm_x_cptr[0] == L->tm_x_ptr) ? 1 : 0;  // keep the other slot
+            hit = L->tm_x_next;
+            L->tm_x_next = (L->tm_x_next + 1) % perseus_layer::kTmCache;
             L->tm_x_c[hit] = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H));
             L->tm_xg_c[hit] = make_tmap(c.x, uint64_t(L->S), uint64_t(L->H), 1);
             L->tm_x_cptr[hit] = c.x;
@@ -779,7 +784,9 @@ int perseus_layer_forward_host_async(perseus_layer* L, const void* x_host, void*
         if (!L->up) {
             ck(cudaStreamCreateWithFlags(&L->up, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&L->down, cudaStreamNonBlocking), "stream");
-            for (int i = 0; i < 2; ++i) {
+            static const int slots_env = [] { const char* e = getenv("PERSEUS_HOST_SLOTS"); return e ? atoi(e) : 0; }();
+            L->host_slots = slots_env >= 2 ? std::min(slots_env, int(perseus_layer::kHostSlots)) : 3;
+            for (int i = 0; i < L->host_slots; ++i) {
                 ck(cudaMalloc(&L->xs2[i], bytes), "cudaMalloc");
                 ck(cudaMalloc(&L->os2[i], bytes), "cudaMalloc");
                 for (cudaEvent_t* e : {&L->ev_up[i], &L->ev_fwd[i], &L->ev_down[i]}) {
@@ -788,7 +795,7 @@ int perseus_layer_forward_host_async(perseus_layer* L, const void* x_host, void*
                 }
             }
         }
-        const int s = int(L->host_calls++ & 1);
+        const int s = int(L->host_calls++ % uint64_t(L->host_slots));
         // upload: after the forward that last read this slot
         ck(cudaStreamWaitEvent(L->up, L->ev_fwd[s], 0), "wait");
         ck(cudaMemcpyAsync(L->xs2[s], x_host, bytes, cudaMemcpyHostToDevice, L->up), "H2D x");
