@@ -53,44 +53,56 @@ void launch_synth_fill(bf16* out, uint64_t base, uint64_t first, uint64_t n, flo
 // (16 independent chains).  128-deep h steps staged through shared memory (fp32,
 // h-major), the next step's tiles loaded into registers while the current one
 // is consumed, so the global load latency hides under 2048 FMAs per thread.
-constexpr int kGateT = 64, kGateE = 64, kGateH = 128;
-constexpr size_t kGateSmem = sizeof(float) * kGateH * (kGateT + kGateE);
+constexpr int kGateE = 64, kGateH = 128;
+template <int TT>  // tokens per thread (the CTA tile is 8 * TT tokens x 64 experts)
+constexpr size_t gate_smem() { return sizeof(float) * kGateH * (8 * TT + kGateE); }
 
+template <int TT>
 __global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const bf16* __restrict__ wg,
                                               float* __restrict__ logits, int S, int H, int E) {
+    constexpr int kT = 8 * TT;            // tokens per CTA: warp w has tokens w * TT + [0, TT)
     extern __shared__ __align__(16) float gsm[];
-    float* xs = gsm;                      // [kGateH][kGateT]
-    float* ws = gsm + kGateH * kGateT;    // [kGateH][kGateE]
+    float* xs = gsm;                      // [kGateH][kT]
+    float* ws = gsm + kGateH * kT;        // [kGateH][kGateE]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int t0 = blockIdx.x * kGateT, e0 = blockIdx.y * kGateE;
-    float acc[8][2];
+    const int t0 = blockIdx.x * kT, e0 = blockIdx.y * kGateE;
+    float acc[TT][2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.f;
+    for (int q = 0; q < TT; ++q) acc[q][0] = acc[q][1] = 0.f;
 
-    // loader: row tid % 64 (a warp = 32 consecutive rows: conflict-free h-major
-    // stores), 8-wide h chunks (tid / 64) + 4 i of the 16 in a step
-    const int lr = tid & 63, lc = tid >> 6;
-    const bool xr = t0 + lr < S, wr = e0 + lr < E;
-    uint4 px[4], pw[4];
+    // loader: x rows tid % kT with 8-wide h chunks (tid / kT) + (256 / kT) i; w rows
+    // tid % 64 with chunks (tid / 64) + 4 i — a warp stores 32 consecutive rows of
+    // one h (conflict-free h-major staging)
+    constexpr int kXC = 256 / kT, kXN = 16 / kXC;  // x: chunk stride, chunks per thread
+    const int xr = tid % kT, xc = tid / kT, wr = tid & 63, wc = tid >> 6;
+    const bool xok = t0 + xr < S, wok = e0 + wr < E;
+    uint4 px[kXN], pw[4];
     auto fetch = [&](int h0) {
 #pragma unroll
+        for (int i = 0; i < kXN; ++i) {
+            const int h = h0 + (xc + kXC * i) * 8;
+            px[i] = xok && h < H ? *reinterpret_cast<const uint4*>(x + size_t(t0 + xr) * H + h) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int h = h0 + (lc + 4 * i) * 8;
-            px[i] = xr && h < H ? *reinterpret_cast<const uint4*>(x + size_t(t0 + lr) * H + h) : make_uint4(0, 0, 0, 0);
-            pw[i] = wr && h < H ? *reinterpret_cast<const uint4*>(wg + size_t(e0 + lr) * H + h) : make_uint4(0, 0, 0, 0);
+            const int h = h0 + (wc + 4 * i) * 8;
+            pw[i] = wok && h < H ? *reinterpret_cast<const uint4*>(wg + size_t(e0 + wr) * H + h) : make_uint4(0, 0, 0, 0);
         }
     };
     auto stage = [&]() {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int hh = (lc + 4 * i) * 8;
+        for (int i = 0; i < kXN; ++i) {
+            const int hh = (xc + kXC * i) * 8;
             const bf16* b = reinterpret_cast<const bf16*>(&px[i]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) xs[(hh + q) * kT + xr] = __bfloat162float(b[q]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int hh = (wc + 4 * i) * 8;
             const bf16* c = reinterpret_cast<const bf16*>(&pw[i]);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                xs[(hh + q) * kGateT + lr] = __bfloat162float(b[q]);
-                ws[(hh + q) * kGateE + lr] = __bfloat162float(c[q]);
-            }
+            for (int q = 0; q < 8; ++q) ws[(hh + q) * kGateE + wr] = __bfloat162float(c[q]);
         }
     };
     fetch(0);
@@ -101,12 +113,15 @@ __global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const 
         const int hn = min(kGateH, H - h0);
 #pragma unroll 8
         for (int h = 0; h < hn; ++h) {
-            const float4 xa = *reinterpret_cast<const float4*>(&xs[h * kGateT + warp * 8]);
-            const float4 xb = *reinterpret_cast<const float4*>(&xs[h * kGateT + warp * 8 + 4]);
-            const float2 wv = *reinterpret_cast<const float2*>(&ws[h * kGateE + lane * 2]);
-            const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+            float xv[TT];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < TT; q += 4) {
+                const float4 xa = *reinterpret_cast<const float4*>(&xs[h * kT + warp * TT + q]);
+                xv[q] = xa.x; xv[q + 1] = xa.y; xv[q + 2] = xa.z; xv[q + 3] = xa.w;
+            }
+            const float2 wv = *reinterpret_cast<const float2*>(&ws[h * kGateE + lane * 2]);
+#pragma unroll
+            for (int q = 0; q < TT; ++q) {
                 acc[q][0] = __fmaf_rn(xv[q], wv.x, acc[q][0]);
                 acc[q][1] = __fmaf_rn(xv[q], wv.y, acc[q][1]);
             }
@@ -114,8 +129,8 @@ __global__ void __launch_bounds__(256) k_gate(const bf16* __restrict__ x, const 
         __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int t = t0 + warp * 8 + q;
+    for (int q = 0; q < TT; ++q) {
+        const int t = t0 + warp * TT + q;
         if (t >= S) continue;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -664,9 +679,11 @@ __global__ void __launch_bounds__(1024) k_combine(DevCtx c) {
 
 // ------------------------------------------------------------- launchers ----
 // bit-exact CUDA-core gate (learned-gate routing)
+// (8 tokens per thread; 4 per thread — 32-token tiles, twice the warps per SM —
+// was bit-identical but 117 vs 95 us)
 void launch_gate_exact(const DevCtx& c, cudaStream_t st) {
-    dim3 g((c.S + kGateT - 1) / kGateT, (c.E + kGateE - 1) / kGateE);
-    k_gate<<<g, 256, kGateSmem, st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
+    dim3 g((c.S + 63) / 64, (c.E + kGateE - 1) / kGateE);
+    k_gate<8><<<g, 256, gate_smem<8>(), st>>>(c.x, c.wg, c.logits, c.S, c.H, c.E);
 }
 
 // the per-forward plan (plan.cuh), one CTA of 8 warps
@@ -799,7 +816,7 @@ static cudaError_t combine_carveouts() {
 cudaError_t configure_kernels(const DevCtx& c) {
     cudaError_t e = cudaFuncSetAttribute(k_plan4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan_smem_bytes(c)));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGateSmem));
+    e = cudaFuncSetAttribute(k_gate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gate_smem<8>()));
     if (e != cudaSuccess) return e;
     for (auto f : {k_perm<8, false>, k_perm<8, true>, k_perm<0, false>, k_perm<0, true>}) {
         e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -809,7 +826,7 @@ cudaError_t configure_kernels(const DevCtx& c) {
         if (e != cudaSuccess) return e;
     }
     const cudaError_t es[] = {max_carveout(k_route), max_carveout(k_plan4), max_carveout(k_dispatch),
-                              max_carveout(k_gate), max_carveout(k_synth_fill), combine_carveouts<1, false>(),
+                              max_carveout(k_gate<8>), max_carveout(k_synth_fill), combine_carveouts<1, false>(),
                               combine_carveouts<2, false>(), combine_carveouts<1, true>(), combine_carveouts<2, true>()};
     for (cudaError_t x : es)
         if (x != cudaSuccess) return x;
