@@ -101,6 +101,7 @@ struct DevCtx {
     int32_t local_dispatch;     // compute-only twin: dispatch puts / flags stay local, remote tiles not awaited
     int32_t local_combine;      // compute-only twin: combine puts / flags stay local, combine flags not awaited
     int32_t pdl;                // launch with programmatic dependent launch (PERSEUS_F_NO_PDL clears it)
+    int32_t snake;              // plan: odd remote classes' pairs in descending expert order (L2 reuse)
 };
 
 // kernel ids of the diagnostic timeline (DevCtx::tl)

@@ -94,6 +94,13 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     int32_t* rp = sp + E;       // recv position per (ks, j)
     int32_t* pp = rp + E;       // pair position per (class, j): class = arrival index of a pair's later tile
     int32_t* selfo = pp + E;    // [El] self-segment row offsets
+    // Pair order inside a remote class: experts ascending in even classes and
+    // descending in odd ones (c.snake, per-destination signalling only — the
+    // whole class lands at once).  Consecutive classes then meet on the same
+    // experts, whose weights the previous class left in L2 (P >= 2: each expert's
+    // weights are streamed once per class).
+    const bool snake = c.snake && c.group_size == 0;
+    auto pslot = [&](int a, int j) { return snake && (a & 1) ? El - 1 - j : j; };
     __shared__ int32_t s_err, s_total_tiles, s_rows_in, s_n_send, s_n_recv, s_n_pairs;
     __shared__ int32_t dst_first[kMaxPes], dst_n[kMaxPes], dst_group[kMaxPes], n_dgroups;
     __shared__ int32_t src_first[kMaxPes], src_n[kMaxPes], src_group[kMaxPes], n_cgroups_pe;
@@ -199,7 +206,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
             #pragma unroll 1
             for (int a = 0; a < P; ++a) n_all += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
             #pragma unroll 1
-            for (int a = 0; a < P; ++a) pp[a * El + j] = 0;
+            for (int a = 0; a < P; ++a) pp[a * El + pslot(a, j)] = 0;
             int a = 0, lim = ceil_tiles(T[r * E + r + P * j]);  // list positions [0, lim) come from class a
             #pragma unroll 1
             for (int m = 0; 2 * m < n_all; ++m) {
@@ -208,7 +215,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                     ++a;
                     lim += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
                 }
-                ++pp[a * El + j];
+                ++pp[a * El + pslot(a, j)];
             }
         }
         const int32_t n_pairs = warp_scan(pp, E);  // class-major pair positions
@@ -412,7 +419,7 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
                     lim += ceil_tiles(T[((r - a + P) % P) * E + r + P * j]);
                     in_cls = 0;
                 }
-                const int q = pp[a * El + j] + in_cls++;
+                const int q = pp[a * El + pslot(a, j)] + in_cls++;
                 const int po = a == 0 ? (q < head ? q : q + (n_pairs - n0)) : head + (q - n0);
                 const int t0 = next_tile();
                 const int t1 = 2 * m + 1 < n_all ? next_tile() : -1;
