@@ -96,10 +96,11 @@ __device__ __forceinline__ void plan_body(const DevCtx& c, int32_t* sm) {
     int32_t* selfo = pp + E;    // [El] self-segment row offsets
     // Pair order inside a remote class: experts ascending in even classes and
     // descending in odd ones (c.snake, per-destination signalling only — the
-    // whole class lands at once).  Consecutive classes then meet on the same
-    // experts, whose weights the previous class left in L2 (P >= 2: each expert's
-    // weights are streamed once per class).
-    const bool snake = c.snake && c.group_size == 0;
+    // whole class lands at once; not with token dedup, whose receiver expands a
+    // class's tiles in ascending order).  Consecutive classes then meet on the
+    // same experts, whose weights the previous class left in L2 (P >= 2: each
+    // expert's weights are streamed once per class).
+    const bool snake = c.snake && c.group_size == 0 && !c.dedup;
     auto pslot = [&](int a, int j) { return snake && (a & 1) ? El - 1 - j : j; };
     __shared__ int32_t s_err, s_total_tiles, s_rows_in, s_n_send, s_n_recv, s_n_pairs;
     __shared__ int32_t dst_first[kMaxPes], dst_n[kMaxPes], dst_group[kMaxPes], n_dgroups;
