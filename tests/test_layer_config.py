@@ -44,3 +44,39 @@ def test_auto_group_size(P, S, want):
 
 def test_per_tile_protocols_report_group_size_one():
     assert pb.resolve_group_size(QWEN3, 4096, 4, protocol=pb.vanilla_protocol()) == 0
+
+
+def test_pdl_off_when_ranks_share_a_device(monkeypatch):
+    """MoELayer(pdl=None): PERSEUS_F_NO_PDL is set when the EP world is larger than
+    the visible device count (several ranks per GPU: a grid waiting for its PDL
+    primary holds up the work distributor) or PERSEUS_SHARED_DEVICE=1, never for
+    one process per GPU; pdl=True / False override.  The create call is
+    intercepted, so no GPU is needed."""
+    import torch
+    from paper_2605_00686_b200 import _lib, layer as layer_mod
+    seen = []
+
+    class FakeLib:
+        def __getattr__(self, name):
+            return getattr(_lib.lib, name)
+
+        @staticmethod
+        def perseus_layer_create(cfg, rank, world, device, h):
+            seen.append(cfg._obj.flags)
+            return 0
+
+    monkeypatch.setattr(layer_mod, "lib", FakeLib())
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 4)
+    monkeypatch.delenv("PERSEUS_SHARED_DEVICE", raising=False)
+
+    def flags_for(world, **kw):
+        seen.clear()
+        layer_mod.MoELayer(QWEN3, 1024, rank=0, world=world, **kw)
+        return seen[-1]
+
+    assert not flags_for(4) & _lib.F_NO_PDL          # one process per GPU
+    assert flags_for(8) & _lib.F_NO_PDL              # 8 ranks on 4 GPUs
+    assert not flags_for(8, pdl=True) & _lib.F_NO_PDL
+    assert flags_for(2, pdl=False) & _lib.F_NO_PDL
+    monkeypatch.setenv("PERSEUS_SHARED_DEVICE", "1")
+    assert flags_for(2) & _lib.F_NO_PDL
